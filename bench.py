@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""Dose-evaluation benchmark: d = A.x over the native-encoding DDM on 1..N B200s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--accum exact|fp32]
+    python bench.py --impl reference ...      # the reference's own CPU path (oracle/_ref)
+
+One step = one dose evaluation over the whole matrix (every rank's row shard).  Workload (N=1):
+BASELINE.json configs[1], C2 = 8M voxels x 40k spots, ~3.2e9 nnz, binary16 values, u16 indices,
+generated on the device (the reference's serial host generator would take ~7 min); x =
+ddm::seeded_vector(40000, 42).  The matrix (12.9 GB) is ~100x the 126 MB L2, so no flush is
+needed between steps ("inputs larger than L2").
+
+value    = SpMV effective GB/s = sum over ranks of ddm::traffic(dims, layout_of) bytes / step
+           time (max over ranks, CUDA events, device-resident x/d).
+e2e      = same metric through the public API with pinned HOST x and d: H2D x + kernels +
+           D2H d inside the timed region.
+roofline = the dominant kernel's algorithmic bytes / its CUDA-event duration vs the measured
+           HBM copy peak (MEASURED_PEAKS.json).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c4", "c5"])
+    ap.add_argument("--accum", default="exact", choices=["exact", "fp32"])
+    ap.add_argument("--rows", type=int, default=0, help="override rows (testing)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-rows", type=int, default=250_000)
+    ap.add_argument("--e2e-steps", type=int, default=0, help="default: min(steps, 10)")
+    return ap.parse_args()
+
+
+def workload(cfg: str, rows_override: int = 0):
+    from paper_2103_09683_b200 import profiles as P
+    if cfg == "c1":
+        ps = [P.c1()]
+    elif cfg == "c2":
+        ps = [P.c2()]
+    elif cfg == "c4":
+        ps = P.c4_beams()
+    else:  # c5: one scenario (the per-scenario evaluation)
+        ps = [P.c5_scenarios()[0]]
+    if rows_override:
+        for p in ps:
+            p.rows = rows_override
+    return ps
+
+
+def workload_desc(cfg, ps):
+    return {"c1": "C1 synthetic DDM 1M voxels x 4,096 spots ~1% (configs[0])",
+            "c2": "C2 clinical-scale synthetic DDM 8M voxels x 40k spots ~3.2e9 nnz, skewed "
+                  "(configs[1])",
+            "c4": "C4 6-beam hstack 2.97M voxels x 196,608 spots, U32 indices (configs[3])",
+            "c5": "C5 one robust scenario 88M voxels x 40k spots (configs[4])"}[cfg]
+
+
+def measured_hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.rows = []
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(device)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------- CPU baselines ------
+def cpu_reference_run(ps, sample_rows: int, reps: int, warmup: int) -> dict:
+    """The reference's own CPU dose path, unmodified (oracle/_ref = /root/reference/proj built
+    by oracle/Makefile): ddm::generate on a row sample of the workload's profile, then
+    ddm::run_bench(RowChunk, lane_width 32, workers = all host threads) -- bench.cpp:38-103."""
+    from oracle.oracle import Oracle, Profile, have_reference, traffic_bytes
+    cores = os.cpu_count() or 1
+    kind = "reference" if have_reference() else "port"
+    orc = Oracle(kind)
+    sub = [Profile(sample_rows, p.cols, p.target_nnz_ratio, p.empty_row_fraction,
+                   p.row_length_log_mean, p.row_length_log_sigma, p.locality_window, p.seed)
+           for p in ps]
+    parts = [orc.generate(p) for p in sub]
+    m = parts[0] if len(parts) == 1 else hstack(parts)
+    if kind == "reference":
+        r = orc.run_bench(m, algorithm=1, lane_width=32, workers=cores, reps=reps,
+                          warmup=warmup, vector_seed=42)
+        mean_s = r["mean_seconds"]
+    else:
+        import numpy as np
+        x = orc.seeded_vector(m.cols, 42)
+        for _ in range(warmup):
+            orc.spmv_rowchunk(m, x, 32, cores)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            orc.spmv_rowchunk(m, x, 32, cores)
+        mean_s = (time.perf_counter() - t0) / reps
+        del np
+    vb, ib = 2, (2 if m.cols < 65536 else 4)
+    b = traffic_bytes(m.rows, m.cols, m.nnz, vb, ib)
+    return {"value": b / mean_s / 1e9, "unit": "GB/s", "cores": cores, "kind": kind,
+            "ms_per_eval": mean_s * 1e3, "model_bytes": b,
+            "sample": f"ddm::generate rows={sample_rows} of the workload profile "
+                      f"({m.nnz} nnz, {b / 1e9:.3f} GB model bytes), ddm::run_bench rowchunk "
+                      f"L=32 workers={cores}, reps={reps} warmup={warmup}"}
+
+
+def hstack(parts):
+    """Column-wise hstack of per-beam CSR matrices (C4's multi-beam plan)."""
+    import numpy as np
+    from oracle.oracle import U32, Csr
+    rows = parts[0].rows
+    off, lens = 0, []
+    for p in parts:
+        lens.append(np.diff(p.row_ptr.astype(np.int64)))
+    tot = np.sum(lens, axis=0)
+    rp = np.zeros(rows + 1, dtype=np.uint64)
+    np.cumsum(tot, out=rp[1:])
+    col = np.empty(int(rp[-1]), dtype=np.uint32)
+    val = np.empty(int(rp[-1]), dtype=parts[0].values.dtype)
+    pos = rp[:-1].astype(np.int64).copy()
+    for p, ln in zip(parts, lens):
+        for r in np.nonzero(ln)[0]:
+            s, e = int(p.row_ptr[r]), int(p.row_ptr[r + 1])
+            col[pos[r]:pos[r] + e - s] = p.col[s:e] + off
+            val[pos[r]:pos[r] + e - s] = p.values[s:e]
+            pos[r] += e - s
+        off += p.cols
+    return Csr(rows, off, parts[0].precision, U32, rp, col, val)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    ps = workload(args.config, args.rows)
+    r = cpu_reference_run(ps, args.cpu_sample_rows, max(args.steps, 1), max(args.warmup, 0))
+    line = {"impl": "reference", "metric": metric_name(args.config), "value": r["value"],
+            "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": r["ms_per_eval"], "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator)",
+            "config": {"workload": workload_desc(args.config, ps), "sample_rows": args.cpu_sample_rows},
+            "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": r["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def metric_name(cfg):
+    return "SpMV effective GB/s per dose eval (ms per dose eval in ms_per_step)"
+
+
+# ---------------------------------------------------------------------- our arm ------------
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_2103_09683_b200 as dg
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    ps = workload(args.config, args.rows)
+    rows, cols = ps[0].rows, sum(p.cols for p in ps)
+    accum = dg.ACCUM_EXACT if args.accum == "exact" else dg.ACCUM_FP32
+    t0 = time.time()
+    if world > 1:  # nnz-balanced contiguous row shards (8(e)), from the generator's lengths
+        lens = dg.generated_row_lengths(ps, 0, rows, device=local)
+        bounds = dg.partition_lengths(lens, world, 2 + (2 if cols < 65536 else 4))
+        r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+    else:
+        r0, r1 = 0, rows
+    eng = dg.DoseEngine.generate(ps, row_begin=r0, row_end=r1, device=local, accumulation=accum)
+    setup_s = time.time() - t0
+    info = eng.info
+    x_host = dg.seeded_vector(cols, 42)
+    x = torch.from_numpy(x_host).cuda()
+    y = torch.empty(info["rows"], dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+
+    def step(profile=False):
+        eng.dose_device(x.data_ptr(), cols, y.data_ptr(), stream=stream, sync=False,
+                        profile=profile)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        dist.barrier()
+
+    # dominant kernel, CUDA events per launch (same stream), right after the timed region
+    prof_steps = min(args.steps, 10)
+    per = {}
+    for _ in range(prof_steps):
+        step(profile=True)
+        for k in eng.kernel_times():
+            d = per.setdefault(k["name"], {"ms": 0.0, "bytes": k["bytes"], "nnz": k["nnz"],
+                                           "rows": k["rows"]})
+            d["ms"] += k["ms"] / prof_steps
+    dom_name, dom = max(per.items(), key=lambda kv: kv[1]["ms"])
+
+    # end to end through the public API: pinned host x and d, H2D + kernels + D2H timed
+    e2e_steps = args.e2e_steps or min(args.steps, 10)
+    xh = torch.from_numpy(x_host).pin_memory()
+    yh = torch.empty(info["rows"], dtype=torch.float64).pin_memory()
+    eng.dose_host_ptrs(xh.data_ptr(), cols, yh.data_ptr(), stream=stream)  # warm
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+    for _ in range(e2e_steps):
+        eng.dose_host_ptrs(xh.data_ptr(), cols, yh.data_ptr(), stream=stream)
+    f1.record()
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1)
+    assert np.array_equal(yh.numpy().view(np.uint64), y.cpu().numpy().view(np.uint64)), \
+        "host-path d differs from device-path d"
+
+    model_bytes = info["model_bytes"]
+    vals = torch.tensor([ms, e2e_ms], dtype=torch.float64, device="cuda")
+    sums = torch.tensor([float(model_bytes), float(info["nnz"]), 8.0 * cols, 8.0 * info["rows"]],
+                        dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+        dist.all_reduce(sums, op=dist.ReduceOp.SUM)
+    ms, e2e_ms = vals.tolist()
+    total_bytes, total_nnz, h2d, d2h = sums.tolist()
+    ms_step = ms / args.steps
+    e2e_step = e2e_ms / e2e_steps
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    peak, peak_kind = measured_hbm_peak()
+    achieved = dom["bytes"] / (dom["ms"] * 1e-3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "dram_bytes_per_launch.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(f"{args.config}:{args.accum}:{dom_name}")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": metric_name(args.config),
+        "value": total_bytes / (ms_step * 1e-3) / 1e9,
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": max(args.warmup, 3),
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64" if accum == dg.ACCUM_EXACT else "f32",
+        "data": "synthetic (row-parallel device generator, reference profile statistics)",
+        "config": {"workload": workload_desc(args.config, ps), "rows": rows, "cols": cols,
+                   "nnz": int(total_nnz), "value_precision": "binary16",
+                   "index_bytes": info["index_bytes"],
+                   "accumulation": "exact fp64, bit-identical to ddm::spmv_rowchunk L=32"
+                   if accum == dg.ACCUM_EXACT else "fp32 (tol 1e-5 * max|d|)",
+                   "parallelism": f"row-shard x{world} (nnz-balanced)",
+                   "model_bytes_per_step": int(total_bytes), "l2": "inputs larger than L2",
+                   "setup_s": round(setup_s, 2)},
+        "frac_of_8TBps": total_bytes / (ms_step * 1e-3) / 8e12,
+        "frac_of_measured_hbm": total_bytes / (ms_step * 1e-3) / 1e9 / peak,
+        "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "bytes_per_launch": dom["bytes"],
+                     "ms_per_launch": dom["ms"],
+                     "share_of_step": dom["ms"] / ms_step,
+                     "kernels": {k: {"ms": round(v["ms"], 4), "bytes": v["bytes"]}
+                                 for k, v in per.items()}},
+        "e2e": {"value": total_bytes / (e2e_step * 1e-3) / 1e9, "unit": "GB/s",
+                "ms_per_step": e2e_step, "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(info["n_kernels"]) * args.steps * world,
+        "clocks": clk,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            r = cpu_reference_run(ps, args.cpu_sample_rows, 5, 1)
+            line["cpu_baseline"] = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as ex:  # reported, never silently replaced
+            line["cpu_baseline"] = {"value": None, "error": str(ex)[:200]}
+    else:
+        line["cpu_baseline"] = None
+    print(json.dumps(line), flush=True)
+    eng.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

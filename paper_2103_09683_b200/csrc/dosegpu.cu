@@ -1,0 +1,541 @@
+// dosegpu.cu -- C-ABI implementation: validation, row plan, one-time native-encoding upload and
+// the dose evaluation (include/dosegpu.h).  No CPU fallback: every dose is computed on the device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "common.cuh"
+#include "handle.cuh"
+#include "spmv_kernels.cuh"
+
+namespace dg {
+
+// ------------------------------------------------------------------------------------------
+// upload-time validation (ddm::validate, src/sparse.cpp:197-255): per row, columns strictly
+// increasing and < cols; every value finite.  Flags are OR-ed into *bad.
+template <typename V, typename I>
+__global__ void k_validate(const uint64_t* __restrict__ rp, const I* __restrict__ col,
+                           const V* __restrict__ val, uint64_t rows, uint64_t cols,
+                           unsigned* __restrict__ bad) {
+  const uint64_t lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t n_warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  unsigned flag = 0;
+  for (uint64_t r = warp; r < rows; r += n_warps) {
+    const uint64_t s = rp[r], e = rp[r + 1];
+    for (uint64_t j = s + lane; j < e; j += 32) {
+      const uint64_t c = col[j];
+      if (c >= cols) flag |= 1u;
+      if (j > s && c <= static_cast<uint64_t>(col[j - 1])) flag |= 2u;
+      if (!isfinite(widen(val[j]))) flag |= 4u;
+    }
+  }
+  flag = __reduce_or_sync(kFull, flag);
+  if (lane == 0 && flag) atomicOr(bad, flag);
+}
+
+__global__ void k_narrow_u32_u16(const uint32_t* __restrict__ in, uint16_t* __restrict__ out,
+                                 uint64_t n, uint64_t cols, unsigned* __restrict__ bad) {
+  unsigned flag = 0;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t c = in[i];
+    if (c >= cols) flag = 1u;
+    out[i] = static_cast<uint16_t>(c);
+  }
+  if (flag) atomicOr(bad, flag);
+}
+
+__global__ void k_widen_u16_u32(const uint16_t* __restrict__ in, uint32_t* __restrict__ out,
+                                uint64_t n) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = in[i];
+}
+
+__global__ void k_rebase(uint64_t* __restrict__ rp, uint64_t n, uint64_t base) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    rp[i] -= base;
+}
+
+int grid_for(uint64_t work_items, int threads, int max_blocks_per_sm) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t need = (work_items + threads - 1) / threads;
+  const uint64_t cap = static_cast<uint64_t>(sms) * max_blocks_per_sm;
+  return static_cast<int>(std::max<uint64_t>(1, std::min(need, cap)));
+}
+
+// ------------------------------------------------------------------------------------------
+int select_device(int32_t want, int* dev_out) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return DG_ERR_NO_DEVICE;
+  }
+  int dev = want;
+  if (dev < 0) DG_CUDA(cudaGetDevice(&dev));
+  if (dev >= n) return DG_ERR_INVALID_CONFIG;
+  cudaDeviceProp prop;
+  DG_CUDA(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major != 10) return DG_ERR_NO_DEVICE;  // built for sm_100a only
+  DG_CUDA(cudaSetDevice(dev));
+  *dev_out = dev;
+  return DG_OK;
+}
+
+int check_options(const dg_options* o) {
+  if (!o) return DG_OK;
+  if (o->struct_size != sizeof(dg_options)) return DG_ERR_INVALID_CONFIG;
+  const uint32_t L = o->lane_width;
+  if (L < 1 || L > 1024 || (L & (L - 1))) return DG_ERR_INVALID_CONFIG;  // spmv.cpp:40-46
+  if (o->accumulation > DG_ACCUM_FP32) return DG_ERR_INVALID_CONFIG;
+  if (o->accumulation == DG_ACCUM_FP32 && L != 32) return DG_ERR_INVALID_CONFIG;
+  return DG_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// Row plan: non-empty rows binned by length.  L = 32: bins len 1 | 2 | 3-4 | 5-8 | 9-16 |
+// 17-32 run G = next_pow2(len) lanes per row; len > 32 runs a warp per row, longest first.
+// Other L: one list of all non-empty rows, G = L lanes (L <= 32) or an L-thread CTA.
+int build_plan(Handle* h, const std::vector<uint64_t>& lens) {
+  std::vector<std::vector<uint32_t>> bins(kNumBins);
+  uint64_t nonempty = 0;
+  for (uint64_t r = 0; r < lens.size(); ++r) {
+    const uint64_t len = lens[r];
+    if (len == 0) continue;
+    ++nonempty;
+    int b;
+    if (h->lane_width != 32) b = kBinGeneral;
+    else if (len == 1) b = 0;
+    else if (len == 2) b = 1;
+    else if (len <= 4) b = 2;
+    else if (len <= 8) b = 3;
+    else if (len <= 16) b = 4;
+    else if (len <= 32) b = 5;
+    else b = kBinLong;
+    bins[b].push_back(static_cast<uint32_t>(r));
+  }
+  // Longest-processing-time order for the warp-per-row bin (no tail of one 40k-nnz row).
+  std::stable_sort(bins[kBinLong].begin(), bins[kBinLong].end(),
+                   [&](uint32_t a, uint32_t b) { return lens[a] > lens[b]; });
+  h->nonempty_rows = nonempty;
+  for (int b = 0; b < kNumBins; ++b) {
+    h->bin_count[b] = static_cast<uint32_t>(bins[b].size());
+    for (uint32_t r : bins[b]) h->bin_nnz[b] += lens[r];
+    if (bins[b].empty()) continue;
+    DG_CUDA(cudaMalloc(&h->d_bin[b], bins[b].size() * 4));
+    DG_CUDA(cudaMemcpy(h->d_bin[b], bins[b].data(), bins[b].size() * 4, cudaMemcpyHostToDevice));
+    h->plan_bytes += bins[b].size() * 4;
+  }
+  return DG_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// Launch one row-list kernel over bin b with G lanes per row (G = 32: warp-per-row loop).
+template <typename K>
+void launch_bin(Handle* h, int b, uint32_t lanes_per_row, const char* name, cudaStream_t s,
+                K kernel) {
+  const uint32_t cnt = h->bin_count[b];
+  if (!cnt) return;
+  kernel(grid_for(static_cast<uint64_t>(cnt) * lanes_per_row, 256), cnt);
+  h->post(s, name, cnt, h->bin_nnz[b]);
+}
+
+template <typename V, typename I>
+int launch_exact(Handle* h, const double* x, double* y, cudaStream_t s) {
+  const uint64_t* rp = h->d_row_ptr;
+  const I* col = static_cast<const I*>(h->d_col);
+  const V* val = static_cast<const V*>(h->d_val);
+  uint32_t* const* bl = h->d_bin;
+#define DG_GROUP(G, B, NAME)                                                                   \
+  launch_bin(h, B, G, NAME, s, [&](int grid, uint32_t cnt) {                                    \
+    k_group_exact<G, V, I><<<grid, 256, 0, s>>>(rp, col, val, x, bl[B], cnt, y);                \
+  })
+  if (h->lane_width == 32) {
+    DG_GROUP(1, 0, "group_exact<1>");
+    DG_GROUP(2, 1, "group_exact<2>");
+    DG_GROUP(4, 2, "group_exact<4>");
+    DG_GROUP(8, 3, "group_exact<8>");
+    DG_GROUP(16, 4, "group_exact<16>");
+    DG_GROUP(32, 5, "group_exact<32>");
+    launch_bin(h, kBinLong, 32, "warp_exact", s, [&](int grid, uint32_t cnt) {
+      k_warp_exact<V, I><<<grid, 256, 0, s>>>(rp, col, val, x, bl[kBinLong], cnt, y);
+    });
+  } else {
+    switch (h->lane_width) {
+      case 1: DG_GROUP(1, kBinGeneral, "group_exact<L=1>"); break;
+      case 2: DG_GROUP(2, kBinGeneral, "group_exact<L=2>"); break;
+      case 4: DG_GROUP(4, kBinGeneral, "group_exact<L=4>"); break;
+      case 8: DG_GROUP(8, kBinGeneral, "group_exact<L=8>"); break;
+      case 16: DG_GROUP(16, kBinGeneral, "group_exact<L=16>"); break;
+      default: {
+        const int L = static_cast<int>(h->lane_width);
+        const uint32_t cnt = h->bin_count[kBinGeneral];
+        if (cnt) {
+          k_block_exact<V, I><<<grid_for(cnt, 1, 16), L, L * sizeof(double), s>>>(
+              rp, col, val, x, bl[kBinGeneral], cnt, y);
+          h->post(s, "block_exact<L>", cnt, h->bin_nnz[kBinGeneral]);
+        }
+      }
+    }
+  }
+#undef DG_GROUP
+  DG_CUDA(cudaGetLastError());
+  return DG_OK;
+}
+
+template <typename V, typename I>
+int launch_fp32(Handle* h, const float* x, double* y, cudaStream_t s) {
+  const uint64_t* rp = h->d_row_ptr;
+  const I* col = static_cast<const I*>(h->d_col);
+  const V* val = static_cast<const V*>(h->d_val);
+  uint32_t* const* bl = h->d_bin;
+#define DG_GROUP(G, B, NAME)                                                                   \
+  launch_bin(h, B, G, NAME, s, [&](int grid, uint32_t cnt) {                                    \
+    k_group_fp32<G, V, I><<<grid, 256, 0, s>>>(rp, col, val, x, bl[B], cnt, y);                 \
+  })
+  DG_GROUP(1, 0, "group_fp32<1>");
+  DG_GROUP(2, 1, "group_fp32<2>");
+  DG_GROUP(4, 2, "group_fp32<4>");
+  DG_GROUP(8, 3, "group_fp32<8>");
+  DG_GROUP(16, 4, "group_fp32<16>");
+  DG_GROUP(32, 5, "group_fp32<32>");
+#undef DG_GROUP
+  launch_bin(h, kBinLong, 32, "warp_fp32", s, [&](int grid, uint32_t cnt) {
+    k_warp_fp32<V, I><<<grid, 256, 0, s>>>(rp, col, val, x, bl[kBinLong], cnt, y);
+  });
+  DG_CUDA(cudaGetLastError());
+  return DG_OK;
+}
+
+template <typename F>
+int dispatch_types(Handle* h, F&& f) {
+  const bool u16 = h->index_bytes == 2;
+  switch (h->value_precision) {
+    case DG_HALF: return u16 ? f(uint16_t{}, uint16_t{}) : f(uint16_t{}, uint32_t{});
+    case DG_SINGLE: return u16 ? f(float{}, uint16_t{}) : f(float{}, uint32_t{});
+    default: return u16 ? f(double{}, uint16_t{}) : f(double{}, uint32_t{});
+  }
+}
+
+int run_kernels(Handle* h, const double* d_x, double* d_y, cudaStream_t s) {
+  h->n_launch = 0;
+  if (h->rows) DG_CUDA(cudaMemsetAsync(d_y, 0, h->rows * sizeof(double), s));
+  if (h->profiling) DG_CUDA(cudaEventRecord(h->kev[0], s));
+  int st;
+  if (h->accumulation == DG_ACCUM_FP32) {
+    if (h->cols) {
+      k_x_to_f32<<<grid_for(h->cols, 256, 2), 256, 0, s>>>(d_x, h->d_xf, h->cols);
+      h->post(s, "x_to_f32", 0, 0);
+    }
+    st = dispatch_types(h, [&](auto v, auto i) {
+      return launch_fp32<decltype(v), decltype(i)>(h, h->d_xf, d_y, s);
+    });
+  } else {
+    st = dispatch_types(h, [&](auto v, auto i) {
+      return launch_exact<decltype(v), decltype(i)>(h, d_x, d_y, s);
+    });
+  }
+  h->n_kernels = h->n_launch;
+  return st;
+}
+
+int finish_create(Handle* h, const std::vector<uint64_t>& lens) {
+  DG_TRY(build_plan(h, lens));
+  DG_CUDA(cudaMalloc(&h->d_x, std::max<uint64_t>(h->cols, 1) * sizeof(double)));
+  DG_CUDA(cudaMalloc(&h->d_y, std::max<uint64_t>(h->rows, 1) * sizeof(double)));
+  if (h->accumulation == DG_ACCUM_FP32)
+    DG_CUDA(cudaMalloc(&h->d_xf, std::max<uint64_t>(h->cols, 1) * sizeof(float)));
+  for (auto& e : h->ev) DG_CUDA(cudaEventCreate(&e));
+  for (auto& e : h->kev) DG_CUDA(cudaEventCreate(&e));
+  return DG_OK;
+}
+
+}  // namespace dg
+
+using dg::Handle;
+
+extern "C" {
+
+int dg_create(const dg_csr_view* v, const dg_options* opts_in, dg_handle** out) {
+  if (!v || !out) return DG_ERR_INVALID_CONFIG;
+  *out = nullptr;
+  dg_options opts;
+  dg_default_options(&opts);
+  if (opts_in) opts = *opts_in;
+  DG_TRY(dg::check_options(&opts));
+  if (v->value_precision > DG_DOUBLE) return DG_ERR_INVALID_CONFIG;
+  if (v->index_bytes != 2 && v->index_bytes != 4) return DG_ERR_INVALID_CONFIG;
+  if (v->col_storage_bytes != 2 && v->col_storage_bytes != 4) return DG_ERR_INVALID_CONFIG;
+  if (v->col_storage_bytes == 2 && v->index_bytes == 4) return DG_ERR_INVALID_CONFIG;
+  if (v->index_bytes == 2 && v->cols >= 65536) return DG_ERR_VALIDATION_FAILURE;  // sparse.cpp:232-233
+  if (v->cols > 0xFFFFFFFFull) return DG_ERR_INDEX_OVERFLOW;
+  const uint64_t r0 = opts.row_begin, r1 = opts.row_end ? opts.row_end : v->rows;
+  if (r0 > r1 || r1 > v->rows) return DG_ERR_INVALID_CONFIG;
+  if (!v->row_ptr || (v->nnz && (!v->col_indices || !v->values))) return DG_ERR_VALIDATION_FAILURE;
+  int dev = 0;
+  DG_TRY(dg::select_device(opts.device, &dev));
+
+  // Row pointers of the shard (host copy drives validation + the plan).
+  const uint64_t n_rows = r1 - r0;
+  std::vector<uint64_t> rp(n_rows + 1);
+  if (v->on_device)
+    DG_CUDA(cudaMemcpy(rp.data(), v->row_ptr + r0, (n_rows + 1) * 8, cudaMemcpyDeviceToHost));
+  else
+    std::memcpy(rp.data(), v->row_ptr + r0, (n_rows + 1) * 8);
+  uint64_t first = 0, last = 0;
+  if (v->on_device) {
+    DG_CUDA(cudaMemcpy(&first, v->row_ptr, 8, cudaMemcpyDeviceToHost));
+    DG_CUDA(cudaMemcpy(&last, v->row_ptr + v->rows, 8, cudaMemcpyDeviceToHost));
+  } else {
+    first = v->row_ptr[0];
+    last = v->row_ptr[v->rows];
+  }
+  if (first != 0 || last != v->nnz) return DG_ERR_VALIDATION_FAILURE;  // sparse.cpp:221-229
+  std::vector<uint64_t> lens(n_rows);
+  for (uint64_t r = 0; r < n_rows; ++r) {
+    if (rp[r + 1] < rp[r]) return DG_ERR_VALIDATION_FAILURE;  // sparse.cpp:222-227
+    lens[r] = rp[r + 1] - rp[r];
+  }
+  const uint64_t base = rp[0], shard_nnz = rp[n_rows] - rp[0];
+
+  Handle* h = new (std::nothrow) Handle();
+  if (!h) return DG_ERR_OUT_OF_MEMORY;
+  h->device = dev;
+  h->rows = n_rows;
+  h->cols = v->cols;
+  h->nnz = shard_nnz;
+  h->row_begin = r0;
+  h->row_end = r1;
+  h->value_precision = v->value_precision;
+  h->value_bytes = v->value_precision == DG_HALF ? 2 : v->value_precision == DG_SINGLE ? 4 : 8;
+  h->index_bytes = v->index_bytes;
+  h->lane_width = opts.lane_width;
+  h->accumulation = opts.accumulation;
+
+  auto fail = [&](int s) { dg_destroy(reinterpret_cast<dg_handle*>(h)); return s; };
+  auto cu = [&](cudaError_t e) { return e == cudaSuccess ? DG_OK : DG_ERR_CUDA_BASE + (int)e; };
+  int st;
+  if ((st = cu(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking)))) return fail(st);
+  if ((st = cu(cudaMalloc(&h->d_bad, sizeof(unsigned))))) return fail(st);
+  if ((st = cu(cudaMemset(h->d_bad, 0, sizeof(unsigned))))) return fail(st);
+
+  // --- one-time upload of the native encoding (no expansion: values stay binary16 bits) ------
+  if ((st = cu(cudaMalloc(&h->d_row_ptr, (n_rows + 1) * 8)))) return fail(st);
+  if ((st = cu(cudaMemcpy(h->d_row_ptr, rp.data(), (n_rows + 1) * 8, cudaMemcpyHostToDevice))))
+    return fail(st);
+  if (base) dg::k_rebase<<<dg::grid_for(n_rows + 1, 256), 256>>>(h->d_row_ptr, n_rows + 1, base);
+  const uint64_t nz = std::max<uint64_t>(shard_nnz, 1);
+  if ((st = cu(cudaMalloc(&h->d_val, nz * h->value_bytes)))) return fail(st);
+  if ((st = cu(cudaMalloc(&h->d_col, nz * h->index_bytes)))) return fail(st);
+  const cudaMemcpyKind kind = v->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  if (shard_nnz) {
+    const char* vsrc = static_cast<const char*>(v->values) + base * h->value_bytes;
+    if ((st = cu(cudaMemcpy(h->d_val, vsrc, shard_nnz * h->value_bytes, kind)))) return fail(st);
+    const char* csrc = static_cast<const char*>(v->col_indices) + base * v->col_storage_bytes;
+    if (v->col_storage_bytes == h->index_bytes) {
+      if ((st = cu(cudaMemcpy(h->d_col, csrc, shard_nnz * h->index_bytes, kind)))) return fail(st);
+    } else {  // ddm keeps u32 in memory even when tagged U16 (sparse.hpp:104): narrow on device
+      const uint64_t chunk = 64ull << 20;
+      uint32_t* stage = nullptr;
+      if ((st = cu(cudaMalloc(&stage, std::min(chunk, shard_nnz) * 4)))) return fail(st);
+      for (uint64_t off = 0; off < shard_nnz && !st; off += chunk) {
+        const uint64_t n = std::min(chunk, shard_nnz - off);
+        st = cu(cudaMemcpy(stage, csrc + off * 4, n * 4, kind));
+        if (!st)
+          dg::k_narrow_u32_u16<<<dg::grid_for(n, 256), 256>>>(
+              stage, static_cast<uint16_t*>(h->d_col) + off, n, h->cols, h->d_bad);
+      }
+      cudaDeviceSynchronize();
+      cudaFree(stage);
+      if (st) return fail(st);
+    }
+  }
+  h->matrix_bytes = (n_rows + 1) * 8 + shard_nnz * (h->value_bytes + h->index_bytes);
+  // --- ddm::validate's per-entry invariants on the device copy --------------------------------
+  st = dg::dispatch_types(h, [&](auto vv, auto ii) {
+    using V = decltype(vv);
+    using I = decltype(ii);
+    dg::k_validate<V, I><<<dg::grid_for(32 * n_rows, 256), 256>>>(
+        h->d_row_ptr, static_cast<const I*>(h->d_col), static_cast<const V*>(h->d_val), n_rows,
+        h->cols, h->d_bad);
+    return cu(cudaGetLastError());
+  });
+  if (st) return fail(st);
+  unsigned bad = 0;
+  if ((st = cu(cudaMemcpy(&bad, h->d_bad, sizeof(unsigned), cudaMemcpyDeviceToHost)))) return fail(st);
+  if (bad) return fail(DG_ERR_VALIDATION_FAILURE);
+  if ((st = dg::finish_create(h, lens))) return fail(st);
+  *out = reinterpret_cast<dg_handle*>(h);
+  return DG_OK;
+}
+
+int dg_destroy(dg_handle* hh) {
+  Handle* h = reinterpret_cast<Handle*>(hh);
+  if (!h) return DG_OK;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  cudaFree(h->d_row_ptr);
+  cudaFree(h->d_col);
+  cudaFree(h->d_val);
+  cudaFree(h->d_x);
+  cudaFree(h->d_xf);
+  cudaFree(h->d_y);
+  cudaFree(h->d_bad);
+  for (auto* b : h->d_bin) cudaFree(b);
+  for (auto e : h->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto e : h->kev)
+    if (e) cudaEventDestroy(e);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+  return DG_OK;
+}
+
+int dg_dose(dg_handle* hh, const double* x, uint64_t x_len, double* y, uint32_t flags,
+            void* stream) {
+  Handle* h = reinterpret_cast<Handle*>(hh);
+  if (!h || (!x && h->cols) || (!y && h->rows)) return DG_ERR_INVALID_CONFIG;
+  if (x_len != h->cols) return DG_ERR_DIMENSION_MISMATCH;  // spmv.cpp:34-38
+  DG_CUDA(cudaSetDevice(h->device));
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : h->stream;
+  const bool x_dev = flags & DG_X_ON_DEVICE, y_dev = flags & DG_Y_ON_DEVICE;
+  const double* d_x = x_dev ? x : h->d_x;
+  double* d_y = y_dev ? y : h->d_y;
+  DG_CUDA(cudaEventRecord(h->ev[0], s));
+  if (!x_dev && h->cols)
+    DG_CUDA(cudaMemcpyAsync(h->d_x, x, h->cols * sizeof(double), cudaMemcpyHostToDevice, s));
+  DG_CUDA(cudaEventRecord(h->ev[1], s));
+  h->profiling = (flags & DG_PROFILE) != 0;
+  DG_TRY(dg::run_kernels(h, d_x, d_y, s));
+  DG_CUDA(cudaEventRecord(h->ev[2], s));
+  if (!y_dev && h->rows)
+    DG_CUDA(cudaMemcpyAsync(y, h->d_y, h->rows * sizeof(double), cudaMemcpyDeviceToHost, s));
+  DG_CUDA(cudaEventRecord(h->ev[3], s));
+  h->timing_valid = false;
+  if (!(flags & DG_NO_SYNC) || !x_dev || !y_dev) {
+    DG_CUDA(cudaStreamSynchronize(s));
+    h->collect_timing();
+  }
+  return DG_OK;
+}
+
+int dg_get_info(const dg_handle* hh, dg_info* info) {
+  const Handle* h = reinterpret_cast<const Handle*>(hh);
+  if (!h || !info) return DG_ERR_INVALID_CONFIG;
+  info->rows = h->rows;
+  info->cols = h->cols;
+  info->nnz = h->nnz;
+  info->row_begin = h->row_begin;
+  info->row_end = h->row_end;
+  info->value_bytes = h->value_bytes;
+  info->index_bytes = h->index_bytes;
+  info->lane_width = h->lane_width;
+  info->accumulation = h->accumulation;
+  info->device_bytes = h->matrix_bytes + h->plan_bytes;
+  info->model_bytes = dg_traffic_bytes(h->rows, h->cols, h->nnz, h->value_bytes, h->index_bytes);
+  info->nonempty_rows = h->nonempty_rows;
+  info->n_kernels = h->n_kernels ? h->n_kernels : h->expected_kernels();
+  info->device = h->device;
+  return DG_OK;
+}
+
+int dg_last_timing(const dg_handle* hh, dg_timing* t) {
+  Handle* h = const_cast<Handle*>(reinterpret_cast<const Handle*>(hh));
+  if (!h || !t) return DG_ERR_INVALID_CONFIG;
+  if (!h->timing_valid) {
+    DG_CUDA(cudaSetDevice(h->device));
+    DG_CUDA(cudaEventSynchronize(h->ev[3]));
+    h->collect_timing();
+  }
+  *t = h->last;
+  return DG_OK;
+}
+
+int dg_copy_rows(const dg_handle* hh, uint64_t r0, uint64_t r1, uint64_t* rp_out,
+                 uint32_t* col_out, void* val_out) {
+  const Handle* h = reinterpret_cast<const Handle*>(hh);
+  if (!h || r0 > r1 || r1 > h->rows) return DG_ERR_INVALID_CONFIG;
+  DG_CUDA(cudaSetDevice(h->device));
+  DG_CUDA(cudaMemcpy(rp_out, h->d_row_ptr + r0, (r1 - r0 + 1) * 8, cudaMemcpyDeviceToHost));
+  const uint64_t b = rp_out[0], n = rp_out[r1 - r0] - b;
+  for (uint64_t i = 0; i <= r1 - r0; ++i) rp_out[i] -= b;
+  if (!n) return DG_OK;
+  DG_CUDA(cudaMemcpy(val_out, static_cast<const char*>(h->d_val) + b * h->value_bytes,
+                     n * h->value_bytes, cudaMemcpyDeviceToHost));
+  if (h->index_bytes == 4) {
+    DG_CUDA(cudaMemcpy(col_out, static_cast<const uint32_t*>(h->d_col) + b, n * 4,
+                       cudaMemcpyDeviceToHost));
+  } else {
+    uint32_t* wide = nullptr;
+    DG_CUDA(cudaMalloc(&wide, n * 4));
+    dg::k_widen_u16_u32<<<dg::grid_for(n, 256), 256>>>(static_cast<const uint16_t*>(h->d_col) + b,
+                                                       wide, n);
+    cudaError_t e = cudaMemcpy(col_out, wide, n * 4, cudaMemcpyDeviceToHost);
+    cudaFree(wide);
+    DG_CUDA(e);
+  }
+  return DG_OK;
+}
+
+int dg_kernel_times(const dg_handle* hh, dg_kernel_time* out, uint32_t cap, uint32_t* n_out) {
+  Handle* h = const_cast<Handle*>(reinterpret_cast<const Handle*>(hh));
+  if (!h || !n_out) return DG_ERR_INVALID_CONFIG;
+  *n_out = 0;
+  if (!h->profiling) return DG_OK;
+  DG_CUDA(cudaSetDevice(h->device));
+  const uint32_t n = std::min<uint32_t>(h->n_launch, Handle::kMaxLaunches);
+  if (n) DG_CUDA(cudaEventSynchronize(h->kev[n]));
+  for (uint32_t i = 0; i < n && i < cap; ++i) {
+    float ms = 0;
+    DG_CUDA(cudaEventElapsedTime(&ms, h->kev[i], h->kev[i + 1]));
+    const auto& l = h->launches[i];
+    std::snprintf(out[i].name, sizeof(out[i].name), "%s", l.name);
+    out[i].ms = ms;
+    out[i].rows = l.rows;
+    out[i].nnz = l.nnz;
+    out[i].bytes = l.rows ? dg_traffic_bytes(l.rows, h->cols, l.nnz, h->value_bytes, h->index_bytes)
+                          : 12ull * h->cols;
+    *n_out = i + 1;
+  }
+  return DG_OK;
+}
+
+int dg_copy_row_ptr(const dg_handle* hh, uint64_t r0, uint64_t r1, uint64_t* rp_out) {
+  const Handle* h = reinterpret_cast<const Handle*>(hh);
+  if (!h || !rp_out || r0 > r1 || r1 > h->rows) return DG_ERR_INVALID_CONFIG;
+  DG_CUDA(cudaSetDevice(h->device));
+  DG_CUDA(cudaMemcpy(rp_out, h->d_row_ptr + r0, (r1 - r0 + 1) * 8, cudaMemcpyDeviceToHost));
+  return DG_OK;
+}
+
+int dg_checksum_bits(const double* v, uint64_t n, int on_device, uint64_t* out) {
+  std::vector<double> host;
+  const double* p = v;
+  if (on_device) {
+    host.resize(n);
+    if (n) DG_CUDA(cudaMemcpy(host.data(), v, n * 8, cudaMemcpyDeviceToHost));
+    p = host.data();
+  }
+  uint64_t hsh = 14695981039346656037ull;  // checksum.hpp:25-35, LSB first
+  for (uint64_t i = 0; i < n; ++i) {
+    uint64_t u;
+    std::memcpy(&u, p + i, 8);
+    for (int k = 0; k < 8; ++k) {
+      hsh ^= static_cast<uint8_t>(u >> (8 * k));
+      hsh *= 1099511628211ull;
+    }
+  }
+  *out = hsh;
+  return DG_OK;
+}
+
+}  // extern "C"

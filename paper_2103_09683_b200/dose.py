@@ -1,0 +1,411 @@
+"""Host-side mirror of the reference's dose API over the C-ABI library ``libdosegpu.so``.
+
+Reference interface mirrored (paths relative to /root/reference/proj):
+
+* ``spmv_rowchunk(m, x, cfg)``  <- ``ddm::spmv_rowchunk`` (include/ddm/spmv.hpp:37, src/spmv.cpp:98-111)
+* ``spmv_oracle(m, x)``         <- ``ddm::spmv_oracle`` (spmv.hpp:29, spmv.cpp:82-96) == rowchunk with
+                                   lane_width 1, evaluated on the device
+* ``RowChunkConfig``            <- ``ddm::RowChunkConfig`` (spmv.hpp:15-18); ``workers`` is accepted
+                                   and, as in the reference, never changes a bit of the output
+* ``CsrMatrix``                 <- ``ddm::CsrMatrix`` (sparse.hpp:93-108)
+* ``Error`` / ``Errc``          <- ``ddm::Error`` / ``ddm::Errc`` (include/ddm/error.hpp:8-41)
+* ``checksum_bits``             <- ``ddm::checksum_bits`` (include/ddm/checksum.hpp:25-35)
+* ``traffic_bytes``             <- ``ddm::traffic(dims_of(m), layout_of(m)).total_bytes()``
+                                   (src/perf_model.cpp:41-54)
+
+Everything numeric runs in CUDA kernels inside libdosegpu.so; there is no CPU fallback, and
+importing this module raises when the library is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdosegpu.so")
+
+HALF, SINGLE, DOUBLE = 0, 1, 2          # ddm::ValuePrecision
+U16, U32 = 0, 1                         # ddm::IndexWidth
+ACCUM_EXACT, ACCUM_FP32 = 0, 1
+X_ON_DEVICE, Y_ON_DEVICE, NO_SYNC, PROFILE = 1, 2, 4, 8
+_VDTYPE = {HALF: np.uint16, SINGLE: np.float32, DOUBLE: np.float64}
+
+
+class Errc(enum.IntEnum):
+    """ddm::Errc (error.hpp:8-25); status code = 1 + value."""
+    DuplicateEntry = 0
+    IndexOverflow = 1
+    ValueOverflow = 2
+    NanInput = 3
+    DimensionMismatch = 4
+    InvalidConfig = 5
+    ZeroTraffic = 6
+    ZeroDuration = 7
+    BadMagic = 8
+    TruncatedFile = 9
+    ValidationFailure = 10
+    UnsupportedVersion = 11
+    ParseError = 12
+    UnsupportedFeature = 13
+    InconsistentProfile = 14
+    IoFailure = 15
+
+
+class Error(RuntimeError):
+    """ddm::Error: carries the status; ``code`` is the Errc for contract errors, else None."""
+
+    def __init__(self, status: int, what: str = ""):
+        self.status = status
+        self.code: Optional[Errc] = Errc(status - 1) if 1 <= status <= 16 else None
+        name = _lib().dg_strerror(status).decode() if _LIB is not None else str(status)
+        if status >= 1000:
+            name += f" (cudaError {status - 1000})"
+        super().__init__(f"{name}: {what}" if what else name)
+
+
+# ---------------------------------------------------------------- ctypes plumbing ---------
+class _View(C.Structure):
+    _fields_ = [("rows", C.c_uint64), ("cols", C.c_uint64), ("nnz", C.c_uint64),
+                ("value_precision", C.c_uint8), ("index_bytes", C.c_uint8),
+                ("col_storage_bytes", C.c_uint8), ("on_device", C.c_uint8),
+                ("row_ptr", C.c_void_p), ("col_indices", C.c_void_p), ("values", C.c_void_p)]
+
+
+class _Options(C.Structure):
+    _fields_ = [("struct_size", C.c_uint32), ("device", C.c_int32), ("lane_width", C.c_uint32),
+                ("accumulation", C.c_uint32), ("row_begin", C.c_uint64), ("row_end", C.c_uint64)]
+
+
+class _Profile(C.Structure):
+    _fields_ = [("rows", C.c_uint64), ("cols", C.c_uint64),
+                ("target_nnz_ratio", C.c_double), ("empty_row_fraction", C.c_double),
+                ("row_length_log_mean", C.c_double), ("row_length_log_sigma", C.c_double),
+                ("locality_window", C.c_uint64), ("seed", C.c_uint64)]
+
+
+class _Info(C.Structure):
+    _fields_ = [("rows", C.c_uint64), ("cols", C.c_uint64), ("nnz", C.c_uint64),
+                ("row_begin", C.c_uint64), ("row_end", C.c_uint64),
+                ("value_bytes", C.c_uint32), ("index_bytes", C.c_uint32),
+                ("lane_width", C.c_uint32), ("accumulation", C.c_uint32),
+                ("device_bytes", C.c_uint64), ("model_bytes", C.c_uint64),
+                ("nonempty_rows", C.c_uint64), ("n_kernels", C.c_uint32), ("device", C.c_int32)]
+
+
+class _Timing(C.Structure):
+    _fields_ = [("ms_h2d", C.c_float), ("ms_kernels", C.c_float), ("ms_d2h", C.c_float),
+                ("ms_total", C.c_float)]
+
+
+class _KernelTime(C.Structure):
+    _fields_ = [("name", C.c_char * 48), ("ms", C.c_float), ("bytes", C.c_uint64),
+                ("rows", C.c_uint64), ("nnz", C.c_uint64)]
+
+
+_LIB: Optional[C.CDLL] = None
+
+# name -> (restype, argtypes); the exported surface of include/dosegpu.h
+_SIGS = {
+    "dg_default_options": (None, [C.POINTER(_Options)]),
+    "dg_create": (C.c_int, [C.POINTER(_View), C.POINTER(_Options), C.POINTER(C.c_void_p)]),
+    "dg_create_generated": (C.c_int, [C.POINTER(_Profile), C.c_uint32, C.c_uint32,
+                                      C.POINTER(_Options), C.POINTER(C.c_void_p)]),
+    "dg_generated_row_lengths": (C.c_int, [C.POINTER(_Profile), C.c_uint32, C.c_uint64,
+                                           C.c_uint64, C.c_int32, C.c_void_p]),
+    "dg_destroy": (C.c_int, [C.c_void_p]),
+    "dg_dose": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint32, C.c_void_p]),
+    "dg_get_info": (C.c_int, [C.c_void_p, C.POINTER(_Info)]),
+    "dg_last_timing": (C.c_int, [C.c_void_p, C.POINTER(_Timing)]),
+    "dg_copy_rows": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
+                               C.c_void_p]),
+    "dg_copy_row_ptr": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p]),
+    "dg_checksum_bits": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int, C.POINTER(C.c_uint64)]),
+    "dg_traffic_bytes": (C.c_uint64, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32]),
+    "dg_partition_rows": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p]),
+    "dg_partition_lengths": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p]),
+    "dg_kernel_times": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.POINTER(C.c_uint32)]),
+    "dg_seeded_vector": (None, [C.c_uint64, C.c_uint64, C.c_void_p]),
+    "dg_strerror": (C.c_char_p, [C.c_int]),
+    "dg_version": (C.c_char_p, []),
+}
+
+
+def _lib() -> C.CDLL:
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing -- build it with "
+                              "`python -c 'import __graft_entry__ as g; g.build()'` "
+                              "(there is no CPU fallback)")
+        lib = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(lib, name)
+            f.restype = res
+            f.argtypes = args
+        _LIB = lib
+    return _LIB
+
+
+def _check(status: int, what: str = "") -> None:
+    if status != 0:
+        raise Error(status, what)
+
+
+# ---------------------------------------------------------------- the data model ----------
+@dataclass
+class CsrMatrix:
+    """ddm::CsrMatrix (sparse.hpp:93-108): u64 row_ptr, u32 col_indices in memory whatever the
+    ``index_width`` tag, values as bit patterns of ``precision``."""
+    rows: int
+    cols: int
+    index_width: int
+    row_ptr: np.ndarray
+    col_indices: np.ndarray
+    values: np.ndarray
+    precision: int = HALF
+
+    @property
+    def nnz(self) -> int:
+        return int(self.row_ptr[-1]) if len(self.row_ptr) else 0
+
+
+@dataclass
+class RowChunkConfig:
+    """ddm::RowChunkConfig (spmv.hpp:15-18)."""
+    lane_width: int = 32
+    workers: int = 1
+
+
+@dataclass
+class Profile:
+    """ddm::MatrixProfile (matgen.hpp:18-27)."""
+    rows: int
+    cols: int
+    target_nnz_ratio: float
+    empty_row_fraction: float
+    row_length_log_mean: float
+    row_length_log_sigma: float
+    locality_window: int
+    seed: int
+
+    def _c(self) -> _Profile:
+        return _Profile(self.rows, self.cols, self.target_nnz_ratio, self.empty_row_fraction,
+                        self.row_length_log_mean, self.row_length_log_sigma,
+                        self.locality_window, self.seed)
+
+
+def _profiles(p) -> tuple:
+    ps = [p] if isinstance(p, Profile) else list(p)
+    arr = (_Profile * len(ps))(*[q._c() for q in ps])
+    return arr, len(ps)
+
+
+def _options(device: int, lane_width: int, accumulation: int, row_begin: int, row_end: int):
+    o = _Options()
+    _lib().dg_default_options(C.byref(o))
+    o.device, o.lane_width, o.accumulation = device, lane_width, accumulation
+    o.row_begin, o.row_end = row_begin, row_end
+    return o
+
+
+# ---------------------------------------------------------------- the engine --------------
+class DoseEngine:
+    """A matrix resident on one GPU (the whole matrix, or a row shard of it).
+
+    Create once (validation, row plan, native-encoding upload), then ``dose(x)`` as often as the
+    optimisation loop needs -- the reference pays these costs inside every spmv_rowchunk call.
+    """
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+        info = _Info()
+        _check(_lib().dg_get_info(self._h, C.byref(info)), "dg_get_info")
+        self.info = {k: getattr(info, k) for k, _ in _Info._fields_}
+
+    # --- constructors ---------------------------------------------------------------------
+    @classmethod
+    def from_csr(cls, m: CsrMatrix, *, lane_width: int = 32, accumulation: int = ACCUM_EXACT,
+                 device: int = -1, row_begin: int = 0, row_end: int = 0) -> "DoseEngine":
+        rp = np.ascontiguousarray(m.row_ptr, dtype=np.uint64)
+        if m.col_indices.dtype == np.uint16:
+            col, csb = np.ascontiguousarray(m.col_indices), 2
+        else:
+            col, csb = np.ascontiguousarray(m.col_indices, dtype=np.uint32), 4
+        val = np.ascontiguousarray(m.values, dtype=_VDTYPE[m.precision])
+        view = _View(m.rows, m.cols, m.nnz, m.precision, 2 if m.index_width == U16 else 4, csb, 0,
+                     rp.ctypes.data, col.ctypes.data, val.ctypes.data)
+        h = C.c_void_p()
+        opts = _options(device, lane_width, accumulation, row_begin, row_end)
+        _check(_lib().dg_create(C.byref(view), C.byref(opts), C.byref(h)), "dg_create")
+        return cls(h)
+
+    @classmethod
+    def from_device_arrays(cls, rows: int, cols: int, nnz: int, precision: int, index_bytes: int,
+                           row_ptr_ptr: int, col_ptr: int, col_storage_bytes: int, val_ptr: int,
+                           **kw) -> "DoseEngine":
+        view = _View(rows, cols, nnz, precision, index_bytes, col_storage_bytes, 1, row_ptr_ptr,
+                     col_ptr, val_ptr)
+        h = C.c_void_p()
+        opts = _options(kw.get("device", -1), kw.get("lane_width", 32),
+                        kw.get("accumulation", ACCUM_EXACT), kw.get("row_begin", 0),
+                        kw.get("row_end", 0))
+        _check(_lib().dg_create(C.byref(view), C.byref(opts), C.byref(h)), "dg_create")
+        return cls(h)
+
+    @classmethod
+    def generate(cls, profiles, *, index_bytes: int = 0, lane_width: int = 32,
+                 accumulation: int = ACCUM_EXACT, device: int = -1, row_begin: int = 0,
+                 row_end: int = 0) -> "DoseEngine":
+        arr, n = _profiles(profiles)
+        h = C.c_void_p()
+        opts = _options(device, lane_width, accumulation, row_begin, row_end)
+        _check(_lib().dg_create_generated(arr, n, index_bytes, C.byref(opts), C.byref(h)),
+               "dg_create_generated")
+        return cls(h)
+
+    # --- the dose -------------------------------------------------------------------------
+    def dose(self, x: np.ndarray, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """d = A.x with host arrays (H2D x, kernels, D2H d)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = out if out is not None else np.empty(self.info["rows"], dtype=np.float64)
+        _check(_lib().dg_dose(self._h, x.ctypes.data, len(x), y.ctypes.data, 0, None), "dg_dose")
+        return y
+
+    def dose_device(self, x_ptr: int, x_len: int, y_ptr: int, stream: int = 0,
+                    sync: bool = True, profile: bool = False) -> None:
+        """d = A.x with device-resident x / y (raw pointers, e.g. torch.Tensor.data_ptr())."""
+        flags = X_ON_DEVICE | Y_ON_DEVICE | (0 if sync else NO_SYNC) | (PROFILE if profile else 0)
+        _check(_lib().dg_dose(self._h, C.c_void_p(x_ptr), x_len, C.c_void_p(y_ptr), flags,
+                              C.c_void_p(stream) if stream else None), "dg_dose")
+
+    def dose_host_ptrs(self, x_ptr: int, x_len: int, y_ptr: int, stream: int = 0) -> None:
+        """d = A.x from (pinned) host pointers -- the end-to-end path."""
+        _check(_lib().dg_dose(self._h, C.c_void_p(x_ptr), x_len, C.c_void_p(y_ptr), 0,
+                              C.c_void_p(stream) if stream else None), "dg_dose")
+
+    def kernel_times(self) -> list:
+        """Per-launch CUDA-event times + algorithmic bytes of the last profiled dose."""
+        buf = (_KernelTime * 16)()
+        n = C.c_uint32()
+        _check(_lib().dg_kernel_times(self._h, buf, 16, C.byref(n)), "dg_kernel_times")
+        return [{"name": buf[i].name.decode(), "ms": buf[i].ms, "bytes": buf[i].bytes,
+                 "rows": buf[i].rows, "nnz": buf[i].nnz} for i in range(n.value)]
+
+    def last_timing(self) -> dict:
+        t = _Timing()
+        _check(_lib().dg_last_timing(self._h, C.byref(t)), "dg_last_timing")
+        return {"ms_h2d": t.ms_h2d, "ms_kernels": t.ms_kernels, "ms_d2h": t.ms_d2h,
+                "ms_total": t.ms_total}
+
+    def row_ptr(self, r0: int = 0, r1: Optional[int] = None) -> np.ndarray:
+        """Shard row pointers [r0, r1] (not rebased)."""
+        r1 = self.info["rows"] if r1 is None else r1
+        rp = np.empty(r1 - r0 + 1, dtype=np.uint64)
+        _check(_lib().dg_copy_row_ptr(self._h, r0, r1, rp.ctypes.data), "dg_copy_row_ptr")
+        return rp
+
+    def copy_rows(self, r0: int, r1: int) -> CsrMatrix:
+        """Rows [r0, r1) of the resident shard back in the reference's host encoding
+        (u32 column indices in memory, value bit patterns)."""
+        ends = self.row_ptr(r0, r1)
+        n = int(ends[-1] - ends[0])
+        prec = {2: HALF, 4: SINGLE, 8: DOUBLE}[self.info["value_bytes"]]
+        rp = np.empty(r1 - r0 + 1, dtype=np.uint64)
+        col = np.empty(max(n, 1), dtype=np.uint32)
+        val = np.empty(max(n, 1), dtype=_VDTYPE[prec])
+        _check(_lib().dg_copy_rows(self._h, r0, r1, rp.ctypes.data, col.ctypes.data,
+                                   val.ctypes.data), "dg_copy_rows")
+        return CsrMatrix(r1 - r0, self.info["cols"], U16 if self.info["index_bytes"] == 2 else U32,
+                         rp, col[:n], val[:n], prec)
+
+    def close(self) -> None:
+        if self._h:
+            _lib().dg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+# ---------------------------------------------------------------- drop-in functions -------
+def spmv_rowchunk(m: CsrMatrix, x: np.ndarray, cfg: RowChunkConfig = RowChunkConfig(),
+                  *, device: int = -1) -> np.ndarray:
+    """ddm::spmv_rowchunk on the GPU: bits equal the reference's for the same lane_width."""
+    if cfg.workers < 1:
+        raise Error(1 + Errc.InvalidConfig, "workers must be >= 1")
+    if len(x) != m.cols:  # spmv.cpp:34-38: checked before the config, as the reference does
+        raise Error(1 + Errc.DimensionMismatch,
+                    f"input vector length {len(x)} != matrix columns {m.cols}")
+    with DoseEngine.from_csr(m, lane_width=cfg.lane_width, device=device) as e:
+        return e.dose(x)
+
+
+def spmv_oracle(m: CsrMatrix, x: np.ndarray, *, device: int = -1) -> np.ndarray:
+    """ddm::spmv_oracle semantics (sequential fp64 per row) == rowchunk with lane_width 1."""
+    return spmv_rowchunk(m, x, RowChunkConfig(lane_width=1), device=device)
+
+
+def checksum_bits(v: np.ndarray) -> int:
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    out = C.c_uint64()
+    _check(_lib().dg_checksum_bits(v.ctypes.data, len(v), 0, C.byref(out)), "dg_checksum_bits")
+    return int(out.value)
+
+
+def checksum_bits_device(ptr: int, n: int) -> int:
+    out = C.c_uint64()
+    _check(_lib().dg_checksum_bits(C.c_void_p(ptr), n, 1, C.byref(out)), "dg_checksum_bits")
+    return int(out.value)
+
+
+def traffic_bytes(rows: int, cols: int, nnz: int, value_bytes: int = 2, index_bytes: int = 2) -> int:
+    return int(_lib().dg_traffic_bytes(rows, cols, nnz, value_bytes, index_bytes))
+
+
+def partition_rows(row_ptr: np.ndarray, parts: int, bytes_per_nnz: int = 4) -> np.ndarray:
+    rp = np.ascontiguousarray(row_ptr, dtype=np.uint64)
+    b = np.empty(parts + 1, dtype=np.uint64)
+    _check(_lib().dg_partition_rows(rp.ctypes.data, len(rp) - 1, bytes_per_nnz, parts,
+                                    b.ctypes.data), "dg_partition_rows")
+    return b
+
+
+def partition_lengths(lengths: np.ndarray, parts: int, bytes_per_nnz: int = 4) -> np.ndarray:
+    ln = np.ascontiguousarray(lengths, dtype=np.uint32)
+    b = np.empty(parts + 1, dtype=np.uint64)
+    _check(_lib().dg_partition_lengths(ln.ctypes.data, len(ln), bytes_per_nnz, parts,
+                                       b.ctypes.data), "dg_partition_lengths")
+    return b
+
+
+def seeded_vector(n: int, seed: int) -> np.ndarray:
+    """ddm::seeded_vector (bench.cpp:31-36): the reference benchmark's x."""
+    out = np.empty(n, dtype=np.float64)
+    _lib().dg_seeded_vector(n, seed, out.ctypes.data)
+    return out
+
+
+def generated_row_lengths(profiles, row_begin: int, row_end: int, device: int = -1) -> np.ndarray:
+    arr, n = _profiles(profiles)
+    out = np.empty(row_end - row_begin, dtype=np.uint32)
+    _check(_lib().dg_generated_row_lengths(arr, n, row_begin, row_end, device, out.ctypes.data),
+           "dg_generated_row_lengths")
+    return out
+
+
+def exported_symbols() -> Sequence[str]:
+    return list(_SIGS)

@@ -1,0 +1,127 @@
+"""CPU suite: the C-ABI library loads, exports exactly what include/dosegpu.h declares, and its
+host-only logic (status strings, perf-model bytes, nnz-balanced partitioner, option checks)
+behaves; on a box without a GPU every compute entry point fails loudly with DG_ERR_NO_DEVICE
+instead of falling back to the CPU."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2103_09683_b200 as dg
+from paper_2103_09683_b200 import dose as D
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "dosegpu.h")).read()
+    return sorted(set(re.findall(r"\b(dg_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = C.CDLL(D.LIB_PATH)
+    declared = header_symbols()
+    assert len(declared) >= 15
+    for name in declared:
+        assert hasattr(lib, name), name
+    # and the Python binding covers the whole declared surface
+    assert set(declared) == set(dg.exported_symbols())
+
+
+def test_library_is_sm100a_only():
+    out = os.popen(f"cuobjdump --list-elf {D.LIB_PATH} 2>&1").read()
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out.replace("sm_100a", ""))
+
+
+def test_exact_kernels_have_no_fma():
+    """-ffp-contract=off semantics (proj/CMakeLists.txt:10-12): the exact dose kernels must issue
+    separate DMUL/DADD, never DFMA."""
+    sass = os.popen(f"cuobjdump -sass {D.LIB_PATH} 2>&1").read()
+    funcs = re.split(r"\n\s*Function : ", sass)
+    exact = [f for f in funcs if re.match(r"\S*k_(warp|group|block)\w*_exact|\S*exact", f)]
+    exact = [f for f in funcs if "exact" in f.split("\n", 1)[0]]
+    assert exact, "no exact kernels found in SASS"
+    for f in exact:
+        name = f.split("\n", 1)[0]
+        assert "DFMA" not in f, name
+        assert "DMUL" in f and "DADD" in f, name
+
+
+def test_strerror_matches_errc_names():
+    lib = D._lib()
+    names = [e.name for e in dg.Errc]
+    for i, n in enumerate(names):
+        assert lib.dg_strerror(i + 1).decode() == n
+    assert lib.dg_strerror(0).decode() == "OK"
+    assert lib.dg_strerror(900).decode() == "NoDevice"
+
+
+def test_traffic_bytes_is_layout_of_model():
+    """perf_model.cpp:41-54 with layout_of: (vb+ib)*nnz + 16*nr + 8*nc."""
+    assert dg.traffic_bytes(1_000_000, 4096, 40_774_090) == 179_129_128
+    assert dg.traffic_bytes(2_970_000, 68_000, 1_480_000_000, 2, 4) == \
+        6 * 1_480_000_000 + 16 * 2_970_000 + 8 * 68_000
+
+
+def _partition_ref(lens, bpn, parts):
+    w = np.concatenate([[0], np.cumsum(np.asarray(lens, dtype=np.int64) * bpn + 16)])
+    total = w[-1]
+    b = [0]
+    for g in range(1, parts):
+        b.append(int(np.argmax(w * parts >= g * total)))
+    b.append(len(lens))
+    return np.array(b, dtype=np.uint64)
+
+
+@pytest.mark.parametrize("parts", [1, 2, 3, 4, 8])
+def test_partition_is_nnz_balanced(parts):
+    rng = np.random.default_rng(parts)
+    lens = np.where(rng.random(5000) < 0.7, 0, np.exp(rng.normal(5, 1.3, 5000)).astype(np.int64))
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    b = dg.partition_rows(rp, parts)
+    assert np.array_equal(b, _partition_ref(lens, 4, parts))
+    assert np.array_equal(b, dg.partition_lengths(lens.astype(np.uint32), parts))
+    assert b[0] == 0 and b[-1] == len(lens) and np.all(np.diff(b.astype(np.int64)) >= 0)
+    loads = [int((rp[b[g + 1]] - rp[b[g]]) * 4 + 16 * (b[g + 1] - b[g])) for g in range(parts)]
+    assert max(loads) - min(loads) <= 2 * (4 * lens.max() + 16)
+
+
+def test_partition_edge_cases():
+    assert list(dg.partition_rows(np.zeros(1, dtype=np.uint64), 4)) == [0, 0, 0, 0, 0]
+    b = dg.partition_rows(np.array([0, 100], dtype=np.uint64), 3)
+    assert b[0] == 0 and b[-1] == 1
+    with pytest.raises(dg.Error) as e:
+        dg.partition_rows(np.array([0, 5, 3], dtype=np.uint64), 2)
+    assert e.value.code == dg.Errc.ValidationFailure
+    with pytest.raises(dg.Error):
+        dg.partition_rows(np.array([0, 1], dtype=np.uint64), 0)
+
+
+def test_default_options_struct():
+    o = D._Options()
+    D._lib().dg_default_options(C.byref(o))
+    assert o.struct_size == C.sizeof(D._Options) == 32
+    assert (o.device, o.lane_width, o.accumulation, o.row_begin, o.row_end) == (-1, 32, 0, 0, 0)
+
+
+def _no_gpu():
+    try:
+        import torch
+        return not torch.cuda.is_available()
+    except Exception:
+        return True
+
+
+@pytest.mark.skipif(not _no_gpu(), reason="checks the no-GPU behaviour")
+def test_no_device_fails_loudly(port):
+    from oracle.oracle import liver_desk
+    m = port.generate(liver_desk())
+    cm = dg.CsrMatrix(m.rows, m.cols, m.index_width, m.row_ptr, m.col, m.values, m.precision)
+    with pytest.raises(dg.Error) as e:
+        dg.spmv_rowchunk(cm, np.zeros(m.cols))
+    assert e.value.status == 900
+    with pytest.raises(dg.Error):
+        dg.DoseEngine.generate(dg.profiles.liver_desk())
