@@ -237,7 +237,10 @@ def run_ours(args):
     x_host = dg.seeded_vector(cols, 42)
     x = torch.from_numpy(x_host).cuda()
     y = torch.empty(info["rows"], dtype=torch.float64, device="cuda")
-    stream = torch.cuda.current_stream().cuda_stream
+    # a real (non-legacy) stream shared by our kernels and the timing events
+    torch_stream = torch.cuda.Stream()
+    torch.cuda.set_stream(torch_stream)
+    stream = torch_stream.cuda_stream
 
     def step(profile=False):
         eng.dose_device(x.data_ptr(), cols, y.data_ptr(), stream=stream, sync=False,

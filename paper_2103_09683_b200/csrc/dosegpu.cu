@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -12,6 +13,7 @@
 #include "common.cuh"
 #include "handle.cuh"
 #include "spmv_kernels.cuh"
+#include "spmv_tiles.cuh"
 
 namespace dg {
 
@@ -120,6 +122,7 @@ int build_plan(Handle* h, const std::vector<uint64_t>& lens) {
     else if (len <= 8) b = 3;
     else if (len <= 16) b = 4;
     else if (len <= 32) b = 5;
+    else if (h->use_tiles) continue;  // plan_tiles owns every row longer than 32
     else b = kBinLong;
     bins[b].push_back(static_cast<uint32_t>(r));
   }
@@ -149,6 +152,34 @@ void launch_bin(Handle* h, int b, uint32_t lanes_per_row, const char* name, cuda
   h->post(s, name, cnt, h->bin_nnz[b]);
 }
 
+// One persistent launch per wave: 2 CTAs per SM pull tiles; wave k continues the segments
+// whose lane partials wave k-1 stored.
+template <typename V, typename I, typename Acc>
+int launch_tiles(Handle* h, const Acc* x, double* y, cudaStream_t s, const char* name) {
+  if (!h->n_waves) return DG_OK;
+  constexpr int kWarps = Handle::kTileWarps;
+  const size_t smem = static_cast<size_t>(h->window_cols) * sizeof(Acc);
+  static bool attr_set = false;  // per (V, I, Acc) instantiation
+  if (!attr_set) {
+    DG_CUDA(cudaFuncSetAttribute(k_tiles<V, I, Acc, kWarps>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    attr_set = true;
+  }
+  DG_CUDA(cudaMemsetAsync(h->d_counters, 0, Handle::kMaxWaves * sizeof(uint32_t), s));
+  for (uint32_t w = 0; w < h->n_waves; ++w) {
+    if (!h->wave_tiles[w]) continue;
+    const int grid = std::min<int>(2 * h->sm_count, static_cast<int>(h->wave_tiles[w]));
+    k_tiles<V, I, Acc, kWarps><<<grid, kWarps * 32, smem, s>>>(
+        static_cast<const I*>(h->d_col), static_cast<const V*>(h->d_val), x,
+        static_cast<const Tile*>(h->d_tiles[w]), h->wave_tiles[w],
+        static_cast<const Segment*>(h->d_segs[w]), static_cast<Acc*>(h->d_state), y,
+        h->d_counters + w);
+    h->post(s, name, h->wave_rows[w], h->wave_nnz[w]);
+  }
+  DG_CUDA(cudaGetLastError());
+  return DG_OK;
+}
+
 template <typename V, typename I>
 int launch_exact(Handle* h, const double* x, double* y, cudaStream_t s) {
   const uint64_t* rp = h->d_row_ptr;
@@ -169,6 +200,7 @@ int launch_exact(Handle* h, const double* x, double* y, cudaStream_t s) {
     launch_bin(h, kBinLong, 32, "warp_exact", s, [&](int grid, uint32_t cnt) {
       k_warp_exact<V, I><<<grid, 256, 0, s>>>(rp, col, val, x, bl[kBinLong], cnt, y);
     });
+    DG_TRY((launch_tiles<V, I, double>(h, x, y, s, "tiles_exact")));
   } else {
     switch (h->lane_width) {
       case 1: DG_GROUP(1, kBinGeneral, "group_exact<L=1>"); break;
@@ -212,6 +244,7 @@ int launch_fp32(Handle* h, const float* x, double* y, cudaStream_t s) {
   launch_bin(h, kBinLong, 32, "warp_fp32", s, [&](int grid, uint32_t cnt) {
     k_warp_fp32<V, I><<<grid, 256, 0, s>>>(rp, col, val, x, bl[kBinLong], cnt, y);
   });
+  DG_TRY((launch_tiles<V, I, float>(h, x, y, s, "tiles_fp32")));
   DG_CUDA(cudaGetLastError());
   return DG_OK;
 }
@@ -249,11 +282,22 @@ int run_kernels(Handle* h, const double* d_x, double* d_y, cudaStream_t s) {
 }
 
 int finish_create(Handle* h, const std::vector<uint64_t>& lens) {
+  DG_CUDA(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device));
+  const char* plan = std::getenv("DG_PLAN");  // "warp": v0 warp-per-row plan (A/B only)
+  h->use_tiles = h->lane_width == 32 && !(plan && std::strcmp(plan, "warp") == 0);
+  h->acc_bytes = h->accumulation == DG_ACCUM_FP32 ? 4 : 8;
+  h->window_cols = kTileSmemBytes / h->acc_bytes;
+  if (const char* tn = std::getenv("DG_TILE_NNZ")) h->tile_nnz = std::strtoull(tn, nullptr, 10);
   DG_TRY(build_plan(h, lens));
-  DG_CUDA(cudaMalloc(&h->d_x, std::max<uint64_t>(h->cols, 1) * sizeof(double)));
+  if (h->use_tiles) DG_TRY(plan_tiles(h, lens));
+  // x staging is padded to a 16-byte multiple: the 1-D TMA moves 16-byte granules
+  DG_CUDA(cudaMalloc(&h->d_x, (std::max<uint64_t>(h->cols, 1) + 4) * sizeof(double)));
+  DG_CUDA(cudaMemset(h->d_x, 0, (std::max<uint64_t>(h->cols, 1) + 4) * sizeof(double)));
   DG_CUDA(cudaMalloc(&h->d_y, std::max<uint64_t>(h->rows, 1) * sizeof(double)));
-  if (h->accumulation == DG_ACCUM_FP32)
-    DG_CUDA(cudaMalloc(&h->d_xf, std::max<uint64_t>(h->cols, 1) * sizeof(float)));
+  if (h->accumulation == DG_ACCUM_FP32) {
+    DG_CUDA(cudaMalloc(&h->d_xf, (std::max<uint64_t>(h->cols, 1) + 8) * sizeof(float)));
+    DG_CUDA(cudaMemset(h->d_xf, 0, (std::max<uint64_t>(h->cols, 1) + 8) * sizeof(float)));
+  }
   for (auto& e : h->ev) DG_CUDA(cudaEventCreate(&e));
   for (auto& e : h->kev) DG_CUDA(cudaEventCreate(&e));
   return DG_OK;
@@ -390,6 +434,12 @@ int dg_destroy(dg_handle* hh) {
   cudaFree(h->d_xf);
   cudaFree(h->d_y);
   cudaFree(h->d_bad);
+  for (uint32_t w = 0; w < Handle::kMaxWaves; ++w) {
+    cudaFree(h->d_tiles[w]);
+    cudaFree(h->d_segs[w]);
+  }
+  cudaFree(h->d_state);
+  cudaFree(h->d_counters);
   for (auto* b : h->d_bin) cudaFree(b);
   for (auto e : h->ev)
     if (e) cudaEventDestroy(e);
@@ -408,11 +458,15 @@ int dg_dose(dg_handle* hh, const double* x, uint64_t x_len, double* y, uint32_t 
   DG_CUDA(cudaSetDevice(h->device));
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : h->stream;
   const bool x_dev = flags & DG_X_ON_DEVICE, y_dev = flags & DG_Y_ON_DEVICE;
-  const double* d_x = x_dev ? x : h->d_x;
+  // The exact tile kernels TMA the x window straight from the caller's device x when it is
+  // 16-byte aligned with a 16-byte multiple length; otherwise x is staged in the padded buffer.
+  const bool x_direct = x_dev && (reinterpret_cast<uintptr_t>(x) % 16 == 0) && (h->cols % 2 == 0);
+  const double* d_x = x_direct ? x : h->d_x;
   double* d_y = y_dev ? y : h->d_y;
   DG_CUDA(cudaEventRecord(h->ev[0], s));
-  if (!x_dev && h->cols)
-    DG_CUDA(cudaMemcpyAsync(h->d_x, x, h->cols * sizeof(double), cudaMemcpyHostToDevice, s));
+  if (!x_direct && h->cols)
+    DG_CUDA(cudaMemcpyAsync(h->d_x, x, h->cols * sizeof(double),
+                            x_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
   DG_CUDA(cudaEventRecord(h->ev[1], s));
   h->profiling = (flags & DG_PROFILE) != 0;
   DG_TRY(dg::run_kernels(h, d_x, d_y, s));

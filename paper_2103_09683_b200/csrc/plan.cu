@@ -1,0 +1,222 @@
+// plan.cu -- the row plan: length bins for short rows, column-windowed tiles for the rest.
+//
+// Replaces the reference's scheduling (parallel_blocks: equal row-count blocks per std::thread,
+// src/spmv.cpp:17-32) with a device-oriented plan built once at dg_create:
+//   * rows with 1 <= len <= 32  -> bins by next_pow2(len), G lanes per row (k_group_*)
+//   * rows with len > 32        -> segments: a row whose column span fits a shared-memory window
+//                                  is one segment; a wider row is cut greedily into position
+//                                  ranges whose column spans fit (wave k = k-th segment of a row)
+//   * per wave, segments sorted by first column and cut into tiles (window <= W columns,
+//     ~kTileNnz nonzeros); inside a tile, longest segment first.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <numeric>
+#include <vector>
+
+#include "common.cuh"
+#include "handle.cuh"
+#include "spmv_tiles.cuh"
+
+namespace dg {
+
+// first / last column of every row (0, 0 for empty rows)
+template <typename I>
+__global__ void k_row_extents(const uint64_t* __restrict__ rp, const I* __restrict__ col,
+                              uint64_t rows, uint2* __restrict__ ext) {
+  for (uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; r < rows;
+       r += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t s = rp[r], e = rp[r + 1];
+    ext[r] = s == e ? make_uint2(0, 0) : make_uint2(col[s], col[e - 1]);
+  }
+}
+
+// Greedy cut of wide rows: a segment starting at column c ends before the first column >= c+Ws.
+template <typename I>
+__global__ void k_split_rows(const uint64_t* __restrict__ rp, const I* __restrict__ col,
+                             const uint32_t* __restrict__ rows, uint32_t n_rows,
+                             const uint64_t* __restrict__ out_off, uint32_t ws,
+                             uint64_t* __restrict__ pos, uint2* __restrict__ cext,
+                             uint32_t* __restrict__ count) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_rows; i += gridDim.x * blockDim.x) {
+    const uint32_t r = rows[i];
+    uint64_t p = rp[r];
+    const uint64_t e = rp[r + 1];
+    uint64_t o = out_off[i];
+    uint32_t k = 0;
+    while (p < e) {
+      const uint64_t c = col[p], lim = c + ws;
+      uint64_t lo = p + 1, hi = e;  // first q in (p, e] with col[q] >= lim (or e)
+      while (lo < hi) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        if (static_cast<uint64_t>(col[mid]) >= lim) hi = mid; else lo = mid + 1;
+      }
+      pos[o + k] = p;
+      cext[o + k] = make_uint2(static_cast<uint32_t>(c), static_cast<uint32_t>(col[lo - 1]));
+      ++k;
+      p = lo;
+    }
+    count[i] = k;
+  }
+}
+
+namespace {
+
+struct HostSeg {
+  uint64_t p0;
+  uint32_t n, row, slot, clo, chi;
+  uint16_t lane0, flags;
+};
+
+template <typename I>
+int plan_tiles_typed(Handle* h, const std::vector<uint64_t>& lens) {
+  const uint64_t rows = h->rows;
+  const uint32_t align = 16u / h->acc_bytes;                  // elements per 16 B (TMA alignment)
+  const uint32_t W = h->window_cols;                          // window capacity (columns)
+  const uint32_t ws = W - align;                              // max segment span
+  std::vector<uint64_t> rp(rows + 1, 0);
+  for (uint64_t r = 0; r < rows; ++r) rp[r + 1] = rp[r] + lens[r];
+
+  // 1. row extents on the device
+  std::vector<uint2> ext(rows);
+  if (rows) {
+    uint2* d_ext = nullptr;
+    DG_CUDA(cudaMalloc(&d_ext, rows * sizeof(uint2)));
+    k_row_extents<I><<<grid_for(rows, 256), 256>>>(h->d_row_ptr, static_cast<const I*>(h->d_col),
+                                                    rows, d_ext);
+    cudaError_t e = cudaMemcpy(ext.data(), d_ext, rows * sizeof(uint2), cudaMemcpyDeviceToHost);
+    cudaFree(d_ext);
+    DG_CUDA(e);
+  }
+
+  // 2. segments: one per narrow long row, greedy cuts for wide rows
+  std::vector<std::vector<HostSeg>> waves(1);
+  std::vector<uint32_t> wide;
+  for (uint64_t r = 0; r < rows; ++r) {
+    if (lens[r] <= 32) continue;
+    const uint32_t c0 = ext[r].x, c1 = ext[r].y;
+    if (static_cast<uint64_t>(c1) - c0 + 1 <= ws) {
+      waves[0].push_back({rp[r], static_cast<uint32_t>(lens[r]), static_cast<uint32_t>(r), 0, c0,
+                          c1, 0, static_cast<uint16_t>(kSegFirst | kSegLast)});
+    } else {
+      wide.push_back(static_cast<uint32_t>(r));
+    }
+  }
+  h->n_split_rows = wide.size();
+  if (!wide.empty()) {
+    std::vector<uint64_t> off(wide.size() + 1, 0);
+    for (size_t i = 0; i < wide.size(); ++i) {
+      const uint64_t span = static_cast<uint64_t>(ext[wide[i]].y) - ext[wide[i]].x + 1;
+      off[i + 1] = off[i] + span / (ws / 2 + 1) + 2;  // each segment but the last covers >= ws cols
+    }
+    const uint64_t total = off.back();
+    uint32_t *d_rows = nullptr, *d_cnt = nullptr;
+    uint64_t *d_off = nullptr, *d_pos = nullptr;
+    uint2* d_cext = nullptr;
+    int st = DG_OK;
+    auto cu = [&](cudaError_t e) { if (st == DG_OK && e != cudaSuccess) st = DG_ERR_CUDA_BASE + (int)e; };
+    cu(cudaMalloc(&d_rows, wide.size() * 4));
+    cu(cudaMalloc(&d_cnt, wide.size() * 4));
+    cu(cudaMalloc(&d_off, (wide.size() + 1) * 8));
+    cu(cudaMalloc(&d_pos, total * 8));
+    cu(cudaMalloc(&d_cext, total * sizeof(uint2)));
+    std::vector<uint64_t> pos(total);
+    std::vector<uint2> cext(total);
+    std::vector<uint32_t> cnt(wide.size());
+    if (st == DG_OK) {
+      cu(cudaMemcpy(d_rows, wide.data(), wide.size() * 4, cudaMemcpyHostToDevice));
+      cu(cudaMemcpy(d_off, off.data(), (wide.size() + 1) * 8, cudaMemcpyHostToDevice));
+      k_split_rows<I><<<grid_for(wide.size(), 128), 128>>>(
+          h->d_row_ptr, static_cast<const I*>(h->d_col), d_rows, static_cast<uint32_t>(wide.size()),
+          d_off, ws, d_pos, d_cext, d_cnt);
+      cu(cudaGetLastError());
+      cu(cudaMemcpy(pos.data(), d_pos, total * 8, cudaMemcpyDeviceToHost));
+      cu(cudaMemcpy(cext.data(), d_cext, total * sizeof(uint2), cudaMemcpyDeviceToHost));
+      cu(cudaMemcpy(cnt.data(), d_cnt, wide.size() * 4, cudaMemcpyDeviceToHost));
+    }
+    cudaFree(d_rows); cudaFree(d_cnt); cudaFree(d_off); cudaFree(d_pos); cudaFree(d_cext);
+    if (st) return st;
+    for (size_t i = 0; i < wide.size(); ++i) {
+      const uint32_t r = wide[i];
+      const uint64_t end = rp[r + 1];
+      for (uint32_t k = 0; k < cnt[i]; ++k) {
+        const uint64_t p = pos[off[i] + k];
+        const uint64_t q = k + 1 < cnt[i] ? pos[off[i] + k + 1] : end;
+        if (waves.size() <= k) waves.resize(k + 1);
+        uint16_t flags = (k == 0 ? kSegFirst : 0) | (k + 1 == cnt[i] ? kSegLast : 0);
+        waves[k].push_back({p, static_cast<uint32_t>(q - p), r, static_cast<uint32_t>(i),
+                            cext[off[i] + k].x, cext[off[i] + k].y,
+                            static_cast<uint16_t>((p - rp[r]) & 31u), flags});
+      }
+    }
+  }
+
+  // 3. tiles per wave
+  const uint64_t xcap = (h->cols + align - 1) / align * align;  // padded x length on device
+  h->n_waves = static_cast<uint32_t>(std::min<size_t>(waves.size(), Handle::kMaxWaves));
+  if (waves.size() > Handle::kMaxWaves) return DG_ERR_UNSUPPORTED_FEATURE;
+  for (uint32_t w = 0; w < h->n_waves; ++w) {
+    auto& S = waves[w];
+    std::stable_sort(S.begin(), S.end(), [](const HostSeg& a, const HostSeg& b) {
+      return a.clo != b.clo ? a.clo < b.clo : a.row < b.row;
+    });
+    std::vector<Tile> tiles;
+    std::vector<Segment> segs;
+    segs.reserve(S.size());
+    uint64_t wave_nnz = 0, wave_rows = 0;
+    size_t i = 0;
+    while (i < S.size()) {
+      const uint32_t xlo = S[i].clo / align * align;
+      uint32_t hi = S[i].chi;
+      uint64_t nnz = 0;
+      size_t j = i;
+      while (j < S.size()) {
+        const uint32_t nhi = std::max(hi, S[j].chi);
+        if (j > i && (static_cast<uint64_t>(nhi) - xlo + 1 > W || nnz + S[j].n > h->tile_nnz)) break;
+        hi = nhi;
+        nnz += S[j].n;
+        ++j;
+      }
+      // longest segment first inside the tile (warps pull segments dynamically)
+      std::stable_sort(S.begin() + i, S.begin() + j,
+                       [](const HostSeg& a, const HostSeg& b) { return a.n > b.n; });
+      uint32_t xlen = (hi - xlo + 1 + align - 1) / align * align;
+      if (xlo + xlen > xcap) xlen = static_cast<uint32_t>(xcap - xlo);
+      tiles.push_back({xlo, xlen, static_cast<uint32_t>(segs.size()),
+                       static_cast<uint32_t>(segs.size() + (j - i))});
+      for (size_t k = i; k < j; ++k) {
+        segs.push_back({S[k].p0, S[k].n, S[k].row, S[k].slot, S[k].lane0, S[k].flags});
+        wave_nnz += S[k].n;
+        wave_rows += (S[k].flags & kSegLast) ? 1 : 0;
+      }
+      i = j;
+    }
+    h->wave_tiles[w] = static_cast<uint32_t>(tiles.size());
+    h->wave_nnz[w] = wave_nnz;
+    h->wave_rows[w] = wave_rows;
+    if (!tiles.empty()) {
+      DG_CUDA(cudaMalloc(&h->d_tiles[w], tiles.size() * sizeof(Tile)));
+      DG_CUDA(cudaMemcpy(h->d_tiles[w], tiles.data(), tiles.size() * sizeof(Tile),
+                         cudaMemcpyHostToDevice));
+      DG_CUDA(cudaMalloc(&h->d_segs[w], segs.size() * sizeof(Segment)));
+      DG_CUDA(cudaMemcpy(h->d_segs[w], segs.data(), segs.size() * sizeof(Segment),
+                         cudaMemcpyHostToDevice));
+      h->plan_bytes += tiles.size() * sizeof(Tile) + segs.size() * sizeof(Segment);
+    }
+  }
+  if (h->n_split_rows) {
+    DG_CUDA(cudaMalloc(&h->d_state, h->n_split_rows * 32 * h->acc_bytes));
+    h->plan_bytes += h->n_split_rows * 32 * h->acc_bytes;
+  }
+  DG_CUDA(cudaMalloc(&h->d_counters, Handle::kMaxWaves * sizeof(uint32_t)));
+  return DG_OK;
+}
+
+}  // namespace
+
+int plan_tiles(Handle* h, const std::vector<uint64_t>& lens) {
+  return h->index_bytes == 2 ? plan_tiles_typed<uint16_t>(h, lens)
+                             : plan_tiles_typed<uint32_t>(h, lens);
+}
+
+}  // namespace dg

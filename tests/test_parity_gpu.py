@@ -244,6 +244,8 @@ def test_config_errors(port):
 def test_validation_failures(port, desk):
     """ddm::validate invariants (sparse.cpp:197-255) enforced at upload."""
     base = desk["liver-desk"]
+    lens = np.diff(base.row_ptr.astype(np.int64))
+    r2 = int(np.nonzero(lens >= 2)[0][3])  # a row with at least two entries
 
     def broken(fn):
         m = Csr(base.rows, base.cols, base.precision, base.index_width, base.row_ptr.copy(),
@@ -252,19 +254,16 @@ def test_validation_failures(port, desk):
         return to_dg(m)
 
     cases = {
-        "col out of range": lambda m: m.col.__setitem__(int(m.row_ptr[100]), m.cols),
-        "unsorted cols": lambda m: m.col.__setitem__(slice(int(m.row_ptr[77]), int(m.row_ptr[77]) + 2),
-                                                     m.col[int(m.row_ptr[77]):int(m.row_ptr[77]) + 2][::-1]),
-        "duplicate col": lambda m: m.col.__setitem__(int(m.row_ptr[77]) + 1, m.col[int(m.row_ptr[77])]),
+        "col out of range": lambda m: m.col.__setitem__(int(m.row_ptr[r2]), m.cols),
+        "unsorted cols": lambda m: m.col.__setitem__(slice(int(m.row_ptr[r2]), int(m.row_ptr[r2]) + 2),
+                                                     m.col[int(m.row_ptr[r2]):int(m.row_ptr[r2]) + 2][::-1]),
+        "duplicate col": lambda m: m.col.__setitem__(int(m.row_ptr[r2]) + 1, m.col[int(m.row_ptr[r2])]),
         "inf value": lambda m: m.values.__setitem__(12, 0x7C00),
         "nan value": lambda m: m.values.__setitem__(13, 0x7E00),
-        "row_ptr decreasing": lambda m: m.row_ptr.__setitem__(5, m.row_ptr[6] + 1),
+        "row_ptr decreasing": lambda m: m.row_ptr.__setitem__(r2, m.row_ptr[r2 + 1] + 1),
     }
     for what, fn in cases.items():
         m = broken(fn)
-        if what == "unsorted cols":
-            s = int(base.row_ptr[77])
-            assert base.row_ptr[78] - base.row_ptr[77] >= 2
         with pytest.raises(dg.Error) as e:
             dg.DoseEngine.from_csr(m)
         assert e.value.code == dg.Errc.ValidationFailure, what
@@ -378,3 +377,61 @@ def test_c2_full_scale_sampled_rows(port):
         for r in np.argsort(lens)[-8:]:
             m = from_dg(e.copy_rows(int(r), int(r) + 1))
             assert bits(y[r]) == bits(port.spmv_rowchunk(m, x, 32, 1))[0]
+
+
+def _wide_row_matrix(port, rows=3000, cols=40_000, seed=5):
+    """Sparse windowed rows + long dense rows wider than one shared-memory window (forcing
+    multi-wave segments with carried lane partials) + rows straddling window boundaries."""
+    rng = np.random.default_rng(seed)
+    lens = np.where(rng.random(rows) < 0.5, 0, rng.integers(1, 3000, rows))
+    lens[rng.choice(rows, 40, replace=False)] = rng.integers(14_000, cols + 1, 40)  # wide, dense
+    lens[:3] = [cols, 13_823, 27_647]
+    rp = np.zeros(rows + 1, dtype=np.uint64)
+    np.cumsum(lens, out=rp[1:])
+    col = np.empty(int(rp[-1]), dtype=np.uint32)
+    for r in range(rows):
+        n = int(lens[r])
+        if n == 0:
+            continue
+        if n >= 4096:
+            lo = int(rng.integers(0, cols - n + 1))
+            c = np.arange(lo, lo + n)
+        else:
+            lo = int(rng.integers(0, cols - 4096 + 1))
+            c = np.sort(rng.choice(4096, n, replace=False)) + lo
+        col[rp[r]:rp[r + 1]] = c
+    vals = (rng.random(len(col)) * 0.999 + 2 ** -14).astype(np.float16).view(np.uint16)
+    return Csr(rows, cols, HALF, U16, rp, col, vals)
+
+
+@pytest.mark.parametrize("tile_nnz", ["4096", "262144"])
+def test_windowed_tiles_with_split_rows_bit_exact(port, monkeypatch, tile_nnz):
+    monkeypatch.setenv("DG_TILE_NNZ", tile_nnz)
+    m = _wide_row_matrix(port)
+    x = port.seeded_vector(m.cols, 42)
+    want = port.spmv_rowchunk(m, x, 32, 4)
+    with dg.DoseEngine.from_csr(to_dg(m)) as e:
+        got = e.dose(x)
+        assert e.info["n_kernels"] >= 3  # short-row bins + >= 2 waves
+    assert np.array_equal(bits(got), bits(want))
+    with dg.DoseEngine.from_csr(to_dg(m), accumulation=dg.ACCUM_FP32) as e:
+        gf = e.dose(x)
+    assert np.max(np.abs(gf - want)) <= FP32_TOL * np.max(np.abs(want))
+
+
+def test_small_tiles_desk_bit_exact(port, golden, desk, monkeypatch):
+    monkeypatch.setenv("DG_TILE_NNZ", "2048")
+    for name in ("liver-desk", "prostate-desk"):
+        m = desk[name]
+        x = port.seeded_vector(m.cols, 42)
+        y = dg.spmv_rowchunk(to_dg(m), x)
+        assert f"{dg.checksum_bits(y):016x}" == golden[name]["rowchunk"]["32"]
+
+
+def test_v0_warp_plan_still_bit_exact(port, golden, desk, monkeypatch):
+    """DG_PLAN=warp selects the v0 warp-per-row plan (kept for A/B measurement)."""
+    monkeypatch.setenv("DG_PLAN", "warp")
+    m = desk["prostate-desk"]
+    x = port.seeded_vector(m.cols, 42)
+    assert f"{dg.checksum_bits(dg.spmv_rowchunk(to_dg(m), x)):016x}" == \
+        golden["prostate-desk"]["rowchunk"]["32"]
