@@ -1,0 +1,97 @@
+"""Row-sharded dose evaluation across GPUs (one process per GPU, torch.distributed plumbing).
+
+SURVEY.md 8(e): rows are independent (``ddm::rowchunk_rows`` keeps no cross-row state,
+src/spmv.cpp:53-67), so the matrix is cut into nnz-balanced contiguous row blocks
+(``dg_partition_lengths``), each GPU holds its block plus a replicated x, and the only collective
+is an all-gather of the dose slices -- used only when the full d must be resident on a device.
+Output bits are identical for any number of GPUs (the row plan is per-row).
+
+The d slices are unequal, so the all-gather pads every slice to the largest shard and compacts
+(NCCL has no allgatherv); ``gather_dose`` does that on whatever backend the process group uses
+(NCCL on B200s, gloo in the CPU tests).
+"""
+from __future__ import annotations
+
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+from .dose import (ACCUM_EXACT, DoseEngine, generated_row_lengths, partition_lengths,
+                   partition_rows)
+
+
+def shard_bounds_from_lengths(lengths: np.ndarray, world: int, bytes_per_nnz: int = 4) -> np.ndarray:
+    """bounds[g]..bounds[g+1] = rows of rank g (balanced on (vb+ib)*len + 16 bytes per row)."""
+    return partition_lengths(lengths, world, bytes_per_nnz)
+
+
+def shard_bounds_from_row_ptr(row_ptr: np.ndarray, world: int, bytes_per_nnz: int = 4) -> np.ndarray:
+    return partition_rows(row_ptr, world, bytes_per_nnz)
+
+
+def gather_dose(y_local, bounds: Sequence[int], group=None):
+    """All-gather unequal d slices into the full d on every rank (torch tensors, same device as
+    y_local).  Pads to the largest slice, gathers, compacts."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    sizes = [int(bounds[g + 1] - bounds[g]) for g in range(world)]
+    cap = max(sizes) if sizes else 0
+    padded = torch.zeros(cap, dtype=y_local.dtype, device=y_local.device)
+    padded[: y_local.numel()] = y_local
+    parts = [torch.empty(cap, dtype=y_local.dtype, device=y_local.device) for _ in range(world)]
+    dist.all_gather(parts, padded, group=group)
+    return torch.cat([parts[g][: sizes[g]] for g in range(world)])
+
+
+class ShardedDose:
+    """This rank's shard of a row-partitioned matrix on its GPU.
+
+    ``local``: a callable (x_device_tensor, y_device_tensor) -> None computing this rank's slice;
+    by default a DoseEngine over the shard generated on the device.
+    """
+
+    def __init__(self, profiles, *, rank: int, world: int, device: int, bounds: np.ndarray,
+                 accumulation: int = ACCUM_EXACT,
+                 local: Optional[Callable] = None):
+        self.rank, self.world, self.device = rank, world, device
+        self.bounds = np.asarray(bounds, dtype=np.uint64)
+        self.row_begin, self.row_end = int(self.bounds[rank]), int(self.bounds[rank + 1])
+        self.engine = None
+        if local is None:
+            self.engine = DoseEngine.generate(profiles, row_begin=self.row_begin,
+                                              row_end=self.row_end, device=device,
+                                              accumulation=accumulation)
+            self.local = self._engine_local
+        else:
+            self.local = local
+
+    @classmethod
+    def for_generated(cls, profiles, *, rank: int, world: int, device: int, **kw) -> "ShardedDose":
+        ps = [profiles] if not isinstance(profiles, (list, tuple)) else list(profiles)
+        cols = sum(p.cols for p in ps)
+        lens = generated_row_lengths(ps, 0, ps[0].rows, device=device)
+        bounds = shard_bounds_from_lengths(lens, world, 2 + (2 if cols < 65536 else 4))
+        return cls(ps, rank=rank, world=world, device=device, bounds=bounds, **kw)
+
+    def _engine_local(self, x, y, stream: int = 0):
+        self.engine.dose_device(x.data_ptr(), x.numel(), y.data_ptr(), stream=stream, sync=False)
+
+    @property
+    def local_rows(self) -> int:
+        return self.row_end - self.row_begin
+
+    def dose(self, x, y_local, *, gather: bool = False, group=None, stream: int = 0):
+        """Local slice into y_local; with gather=True also returns the full d (all-gather)."""
+        if self.engine is not None:
+            self.local(x, y_local, stream)
+        else:
+            self.local(x, y_local)
+        if gather:
+            return gather_dose(y_local, self.bounds, group)
+        return None
+
+    def close(self):
+        if self.engine is not None:
+            self.engine.close()
