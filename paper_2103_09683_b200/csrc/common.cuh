@@ -42,4 +42,40 @@ __device__ __forceinline__ T ld_stream(const T* p) {
   return __ldcs(p);
 }
 
+// ---- matrix element streams ----------------------------------------------------------------
+// SoA: the reference's separate column / value arrays, any value precision and index width.
+template <typename V, typename I>
+struct SoA {
+  using Val = V;
+  using Idx = I;
+  struct Raw {
+    I c;
+    V v;
+  };
+  const I* col;
+  const V* val;
+  __device__ __forceinline__ Raw load(uint64_t j) const { return {ld_stream(col + j), ld_stream(val + j)}; }
+  __device__ __forceinline__ Idx col_at(uint64_t j) const { return col[j]; }
+  __device__ __forceinline__ static I c_of(const Raw& r) { return r.c; }
+  __device__ __forceinline__ static V v_of(const Raw& r) { return r.v; }
+};
+
+// Packed16: the native (binary16 value, u16 column) pair of one nonzero in one 32-bit word,
+// column in the high half.  Same 4 bytes per nonzero as the SoA pair (no expansion), but one
+// 128-byte request serves 32 lanes' positions instead of two 64-byte requests.
+struct Packed16 {
+  using Val = uint16_t;
+  using Idx = uint16_t;
+  using Raw = uint32_t;
+  const uint32_t* w;
+  __device__ __forceinline__ Raw load(uint64_t j) const { return ld_stream(w + j); }
+  __device__ __forceinline__ Idx col_at(uint64_t j) const { return static_cast<uint16_t>(w[j] >> 16); }
+  __device__ __forceinline__ static uint16_t c_of(Raw r) { return static_cast<uint16_t>(r >> 16); }
+  __device__ __forceinline__ static uint16_t v_of(Raw r) { return static_cast<uint16_t>(r & 0xFFFFu); }
+};
+
+__device__ __forceinline__ uint32_t pack16(uint16_t col, uint16_t half_bits) {
+  return (static_cast<uint32_t>(col) << 16) | half_bits;
+}
+
 }  // namespace dg

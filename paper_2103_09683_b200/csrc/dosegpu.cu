@@ -20,9 +20,8 @@ namespace dg {
 // ------------------------------------------------------------------------------------------
 // upload-time validation (ddm::validate, src/sparse.cpp:197-255): per row, columns strictly
 // increasing and < cols; every value finite.  Flags are OR-ed into *bad.
-template <typename V, typename I>
-__global__ void k_validate(const uint64_t* __restrict__ rp, const I* __restrict__ col,
-                           const V* __restrict__ val, uint64_t rows, uint64_t cols,
+template <class M>
+__global__ void k_validate(M mat, const uint64_t* __restrict__ rp, uint64_t rows, uint64_t cols,
                            unsigned* __restrict__ bad) {
   const uint64_t lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
@@ -31,10 +30,11 @@ __global__ void k_validate(const uint64_t* __restrict__ rp, const I* __restrict_
   for (uint64_t r = warp; r < rows; r += n_warps) {
     const uint64_t s = rp[r], e = rp[r + 1];
     for (uint64_t j = s + lane; j < e; j += 32) {
-      const uint64_t c = col[j];
+      const auto el = mat.load(j);
+      const uint64_t c = M::c_of(el);
       if (c >= cols) flag |= 1u;
-      if (j > s && c <= static_cast<uint64_t>(col[j - 1])) flag |= 2u;
-      if (!isfinite(widen(val[j]))) flag |= 4u;
+      if (j > s && c <= static_cast<uint64_t>(mat.col_at(j - 1))) flag |= 2u;
+      if (!isfinite(widen(M::v_of(el)))) flag |= 4u;
     }
   }
   flag = __reduce_or_sync(kFull, flag);
@@ -53,11 +53,23 @@ __global__ void k_narrow_u32_u16(const uint32_t* __restrict__ in, uint16_t* __re
   if (flag) atomicOr(bad, flag);
 }
 
-__global__ void k_widen_u16_u32(const uint16_t* __restrict__ in, uint32_t* __restrict__ out,
-                                uint64_t n) {
+__global__ void k_pack16(const uint16_t* __restrict__ col, const uint16_t* __restrict__ val,
+                         uint32_t* __restrict__ out, uint64_t n) {
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-    out[i] = in[i];
+    out[i] = pack16(col[i], val[i]);
+}
+
+// rows [r0, r1) of the stream back to the reference's host encoding (u32 columns, value bits)
+template <class M>
+__global__ void k_unpack(M mat, uint64_t b, uint64_t n, uint32_t* __restrict__ col,
+                         typename M::Val* __restrict__ val) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const auto e = mat.load(b + i);
+    col[i] = M::c_of(e);
+    val[i] = M::v_of(e);
+  }
 }
 
 __global__ void k_rebase(uint64_t* __restrict__ rp, uint64_t n, uint64_t base) {
@@ -104,9 +116,9 @@ int check_options(const dg_options* o) {
 }
 
 // ------------------------------------------------------------------------------------------
-// Row plan: non-empty rows binned by length.  L = 32: bins len 1 | 2 | 3-4 | 5-8 | 9-16 |
-// 17-32 run G = next_pow2(len) lanes per row; len > 32 runs a warp per row, longest first.
-// Other L: one list of all non-empty rows, G = L lanes (L <= 32) or an L-thread CTA.
+// Row plan, part 1: non-empty rows of length <= 32 binned by next_pow2(len) (lane_width 32),
+// or every non-empty row in one list (other lane widths).  Longer rows: plan_tiles (plan.cu);
+// DG_PLAN=warp keeps the v0 warp-per-row bin instead, longest row first.
 int build_plan(Handle* h, const std::vector<uint64_t>& lens) {
   std::vector<std::vector<uint32_t>> bins(kNumBins);
   uint64_t nonempty = 0;
@@ -122,11 +134,10 @@ int build_plan(Handle* h, const std::vector<uint64_t>& lens) {
     else if (len <= 8) b = 3;
     else if (len <= 16) b = 4;
     else if (len <= 32) b = 5;
-    else if (h->use_tiles) continue;  // plan_tiles owns every row longer than 32
+    else if (h->use_tiles) continue;
     else b = kBinLong;
     bins[b].push_back(static_cast<uint32_t>(r));
   }
-  // Longest-processing-time order for the warp-per-row bin (no tail of one 40k-nnz row).
   std::stable_sort(bins[kBinLong].begin(), bins[kBinLong].end(),
                    [&](uint32_t a, uint32_t b) { return lens[a] > lens[b]; });
   h->nonempty_rows = nonempty;
@@ -142,121 +153,100 @@ int build_plan(Handle* h, const std::vector<uint64_t>& lens) {
 }
 
 // ------------------------------------------------------------------------------------------
-// Launch one row-list kernel over bin b with G lanes per row (G = 32: warp-per-row loop).
-template <typename K>
-void launch_bin(Handle* h, int b, uint32_t lanes_per_row, const char* name, cudaStream_t s,
-                K kernel) {
+template <int G, class M, typename Acc>
+void launch_group(Handle* h, int b, const char* name, cudaStream_t s, const M& mat, const Acc* x,
+                  double* y) {
   const uint32_t cnt = h->bin_count[b];
   if (!cnt) return;
-  kernel(grid_for(static_cast<uint64_t>(cnt) * lanes_per_row, 256), cnt);
+  k_group<G, M, Acc><<<grid_for(static_cast<uint64_t>(cnt) * G, 256), 256, 0, s>>>(
+      mat, h->d_row_ptr, x, h->d_bin[b], cnt, y);
   h->post(s, name, cnt, h->bin_nnz[b]);
 }
 
-// One persistent launch per wave: 2 CTAs per SM pull tiles; wave k continues the segments
-// whose lane partials wave k-1 stored.
-template <typename V, typename I, typename Acc>
-int launch_tiles(Handle* h, const Acc* x, double* y, cudaStream_t s, const char* name) {
+// One persistent launch per wave (one CTA per SM): wave k continues the segments whose lane
+// partials wave k-1 stored.
+template <class M, typename Acc>
+int launch_tiles(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t s,
+                 const char* name) {
   if (!h->n_waves) return DG_OK;
-  constexpr int kWarps = Handle::kTileWarps;
-  const size_t smem = static_cast<size_t>(h->window_cols) * sizeof(Acc);
-  static bool attr_set = false;  // per (V, I, Acc) instantiation
-  if (!attr_set) {
-    DG_CUDA(cudaFuncSetAttribute(k_tiles<V, I, Acc, kWarps>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    attr_set = true;
+  constexpr int kWarps = Handle::kTileWarps, kU = Handle::kTileUnroll;
+  const size_t smem = 2ull * h->window_cols * sizeof(Acc);
+  if (!h->tiles_attr) {  // a handle has one (M, Acc) and one device
+    DG_CUDA(cudaFuncSetAttribute(k_tiles<M, Acc, kWarps, kU>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+    h->tiles_attr = true;
   }
   DG_CUDA(cudaMemsetAsync(h->d_counters, 0, Handle::kMaxWaves * sizeof(uint32_t), s));
+  static const char* const kWaveName[] = {"[w0]", "[w1]", "[w2]", "[w3]", "[w4]", "[w5]",
+                                          "[w6]", "[w7]", "[w8+]"};
   for (uint32_t w = 0; w < h->n_waves; ++w) {
     if (!h->wave_tiles[w]) continue;
-    const int grid = std::min<int>(2 * h->sm_count, static_cast<int>(h->wave_tiles[w]));
-    k_tiles<V, I, Acc, kWarps><<<grid, kWarps * 32, smem, s>>>(
-        static_cast<const I*>(h->d_col), static_cast<const V*>(h->d_val), x,
-        static_cast<const Tile*>(h->d_tiles[w]), h->wave_tiles[w],
+    const int grid = std::min<int>(h->sm_count, static_cast<int>(h->wave_tiles[w]));
+    k_tiles<M, Acc, kWarps, kU><<<grid, kWarps * 32, smem, s>>>(
+        mat, x, static_cast<const Tile*>(h->d_tiles[w]), h->wave_tiles[w],
         static_cast<const Segment*>(h->d_segs[w]), static_cast<Acc*>(h->d_state), y,
-        h->d_counters + w);
-    h->post(s, name, h->wave_rows[w], h->wave_nnz[w]);
+        h->d_counters + w, h->window_cols);
+    (void)name;
+    h->post(s, kWaveName[std::min<uint32_t>(w, 8)], h->wave_rows[w], h->wave_nnz[w]);
   }
   DG_CUDA(cudaGetLastError());
   return DG_OK;
 }
 
-template <typename V, typename I>
-int launch_exact(Handle* h, const double* x, double* y, cudaStream_t s) {
-  const uint64_t* rp = h->d_row_ptr;
-  const I* col = static_cast<const I*>(h->d_col);
-  const V* val = static_cast<const V*>(h->d_val);
-  uint32_t* const* bl = h->d_bin;
-#define DG_GROUP(G, B, NAME)                                                                   \
-  launch_bin(h, B, G, NAME, s, [&](int grid, uint32_t cnt) {                                    \
-    k_group_exact<G, V, I><<<grid, 256, 0, s>>>(rp, col, val, x, bl[B], cnt, y);                \
-  })
+template <class M>
+int launch_exact(Handle* h, const M& mat, const double* x, double* y, cudaStream_t s) {
   if (h->lane_width == 32) {
-    DG_GROUP(1, 0, "group_exact<1>");
-    DG_GROUP(2, 1, "group_exact<2>");
-    DG_GROUP(4, 2, "group_exact<4>");
-    DG_GROUP(8, 3, "group_exact<8>");
-    DG_GROUP(16, 4, "group_exact<16>");
-    DG_GROUP(32, 5, "group_exact<32>");
-    launch_bin(h, kBinLong, 32, "warp_exact", s, [&](int grid, uint32_t cnt) {
-      k_warp_exact<V, I><<<grid, 256, 0, s>>>(rp, col, val, x, bl[kBinLong], cnt, y);
-    });
-    DG_TRY((launch_tiles<V, I, double>(h, x, y, s, "tiles_exact")));
+    launch_group<1>(h, 0, "group<1>", s, mat, x, y);
+    launch_group<2>(h, 1, "group<2>", s, mat, x, y);
+    launch_group<4>(h, 2, "group<4>", s, mat, x, y);
+    launch_group<8>(h, 3, "group<8>", s, mat, x, y);
+    launch_group<16>(h, 4, "group<16>", s, mat, x, y);
+    launch_group<32>(h, 5, "group<32>", s, mat, x, y);
+    if (h->bin_count[kBinLong]) {
+      k_warp<M, double><<<grid_for(32ull * h->bin_count[kBinLong], 256), 256, 0, s>>>(
+          mat, h->d_row_ptr, x, h->d_bin[kBinLong], h->bin_count[kBinLong], y);
+      h->post(s, "warp_v0", h->bin_count[kBinLong], h->bin_nnz[kBinLong]);
+    }
+    DG_TRY(launch_tiles(h, mat, x, y, s, "tiles"));
   } else {
     switch (h->lane_width) {
-      case 1: DG_GROUP(1, kBinGeneral, "group_exact<L=1>"); break;
-      case 2: DG_GROUP(2, kBinGeneral, "group_exact<L=2>"); break;
-      case 4: DG_GROUP(4, kBinGeneral, "group_exact<L=4>"); break;
-      case 8: DG_GROUP(8, kBinGeneral, "group_exact<L=8>"); break;
-      case 16: DG_GROUP(16, kBinGeneral, "group_exact<L=16>"); break;
+      case 1: launch_group<1>(h, kBinGeneral, "group<L=1>", s, mat, x, y); break;
+      case 2: launch_group<2>(h, kBinGeneral, "group<L=2>", s, mat, x, y); break;
+      case 4: launch_group<4>(h, kBinGeneral, "group<L=4>", s, mat, x, y); break;
+      case 8: launch_group<8>(h, kBinGeneral, "group<L=8>", s, mat, x, y); break;
+      case 16: launch_group<16>(h, kBinGeneral, "group<L=16>", s, mat, x, y); break;
       default: {
         const int L = static_cast<int>(h->lane_width);
         const uint32_t cnt = h->bin_count[kBinGeneral];
         if (cnt) {
-          k_block_exact<V, I><<<grid_for(cnt, 1, 16), L, L * sizeof(double), s>>>(
-              rp, col, val, x, bl[kBinGeneral], cnt, y);
-          h->post(s, "block_exact<L>", cnt, h->bin_nnz[kBinGeneral]);
+          k_block_exact<M><<<grid_for(cnt, 1, 16), L, L * sizeof(double), s>>>(
+              mat, h->d_row_ptr, x, h->d_bin[kBinGeneral], cnt, y);
+          h->post(s, "block<L>", cnt, h->bin_nnz[kBinGeneral]);
         }
       }
     }
   }
-#undef DG_GROUP
   DG_CUDA(cudaGetLastError());
   return DG_OK;
 }
 
-template <typename V, typename I>
-int launch_fp32(Handle* h, const float* x, double* y, cudaStream_t s) {
-  const uint64_t* rp = h->d_row_ptr;
-  const I* col = static_cast<const I*>(h->d_col);
-  const V* val = static_cast<const V*>(h->d_val);
-  uint32_t* const* bl = h->d_bin;
-#define DG_GROUP(G, B, NAME)                                                                   \
-  launch_bin(h, B, G, NAME, s, [&](int grid, uint32_t cnt) {                                    \
-    k_group_fp32<G, V, I><<<grid, 256, 0, s>>>(rp, col, val, x, bl[B], cnt, y);                 \
-  })
-  DG_GROUP(1, 0, "group_fp32<1>");
-  DG_GROUP(2, 1, "group_fp32<2>");
-  DG_GROUP(4, 2, "group_fp32<4>");
-  DG_GROUP(8, 3, "group_fp32<8>");
-  DG_GROUP(16, 4, "group_fp32<16>");
-  DG_GROUP(32, 5, "group_fp32<32>");
-#undef DG_GROUP
-  launch_bin(h, kBinLong, 32, "warp_fp32", s, [&](int grid, uint32_t cnt) {
-    k_warp_fp32<V, I><<<grid, 256, 0, s>>>(rp, col, val, x, bl[kBinLong], cnt, y);
-  });
-  DG_TRY((launch_tiles<V, I, float>(h, x, y, s, "tiles_fp32")));
-  DG_CUDA(cudaGetLastError());
-  return DG_OK;
-}
-
-template <typename F>
-int dispatch_types(Handle* h, F&& f) {
-  const bool u16 = h->index_bytes == 2;
-  switch (h->value_precision) {
-    case DG_HALF: return u16 ? f(uint16_t{}, uint16_t{}) : f(uint16_t{}, uint32_t{});
-    case DG_SINGLE: return u16 ? f(float{}, uint16_t{}) : f(float{}, uint32_t{});
-    default: return u16 ? f(double{}, uint16_t{}) : f(double{}, uint32_t{});
+template <class M>
+int launch_fp32(Handle* h, const M& mat, const float* x, double* y, cudaStream_t s) {
+  launch_group<1>(h, 0, "group_f32<1>", s, mat, x, y);
+  launch_group<2>(h, 1, "group_f32<2>", s, mat, x, y);
+  launch_group<4>(h, 2, "group_f32<4>", s, mat, x, y);
+  launch_group<8>(h, 3, "group_f32<8>", s, mat, x, y);
+  launch_group<16>(h, 4, "group_f32<16>", s, mat, x, y);
+  launch_group<32>(h, 5, "group_f32<32>", s, mat, x, y);
+  if (h->bin_count[kBinLong]) {
+    k_warp<M, float><<<grid_for(32ull * h->bin_count[kBinLong], 256), 256, 0, s>>>(
+        mat, h->d_row_ptr, x, h->d_bin[kBinLong], h->bin_count[kBinLong], y);
+    h->post(s, "warp_f32_v0", h->bin_count[kBinLong], h->bin_nnz[kBinLong]);
   }
+  DG_TRY(launch_tiles(h, mat, x, y, s, "tiles_f32"));
+  DG_CUDA(cudaGetLastError());
+  return DG_OK;
 }
 
 int run_kernels(Handle* h, const double* d_x, double* d_y, cudaStream_t s) {
@@ -269,13 +259,9 @@ int run_kernels(Handle* h, const double* d_x, double* d_y, cudaStream_t s) {
       k_x_to_f32<<<grid_for(h->cols, 256, 2), 256, 0, s>>>(d_x, h->d_xf, h->cols);
       h->post(s, "x_to_f32", 0, 0);
     }
-    st = dispatch_types(h, [&](auto v, auto i) {
-      return launch_fp32<decltype(v), decltype(i)>(h, h->d_xf, d_y, s);
-    });
+    st = dispatch_mat(h, [&](const auto& mat) { return launch_fp32(h, mat, h->d_xf, d_y, s); });
   } else {
-    st = dispatch_types(h, [&](auto v, auto i) {
-      return launch_exact<decltype(v), decltype(i)>(h, d_x, d_y, s);
-    });
+    st = dispatch_mat(h, [&](const auto& mat) { return launch_exact(h, mat, d_x, d_y, s); });
   }
   h->n_kernels = h->n_launch;
   return st;
@@ -286,7 +272,7 @@ int finish_create(Handle* h, const std::vector<uint64_t>& lens) {
   const char* plan = std::getenv("DG_PLAN");  // "warp": v0 warp-per-row plan (A/B only)
   h->use_tiles = h->lane_width == 32 && !(plan && std::strcmp(plan, "warp") == 0);
   h->acc_bytes = h->accumulation == DG_ACCUM_FP32 ? 4 : 8;
-  h->window_cols = kTileSmemBytes / h->acc_bytes;
+  h->window_cols = kWindowBytes / h->acc_bytes;
   if (const char* tn = std::getenv("DG_TILE_NNZ")) h->tile_nnz = std::strtoull(tn, nullptr, 10);
   DG_TRY(build_plan(h, lens));
   if (h->use_tiles) DG_TRY(plan_tiles(h, lens));
@@ -403,20 +389,30 @@ int dg_create(const dg_csr_view* v, const dg_options* opts_in, dg_handle** out) 
       if (st) return fail(st);
     }
   }
-  h->matrix_bytes = (n_rows + 1) * 8 + shard_nnz * (h->value_bytes + h->index_bytes);
   // --- ddm::validate's per-entry invariants on the device copy --------------------------------
-  st = dg::dispatch_types(h, [&](auto vv, auto ii) {
-    using V = decltype(vv);
-    using I = decltype(ii);
-    dg::k_validate<V, I><<<dg::grid_for(32 * n_rows, 256), 256>>>(
-        h->d_row_ptr, static_cast<const I*>(h->d_col), static_cast<const V*>(h->d_val), n_rows,
-        h->cols, h->d_bad);
+  st = dg::dispatch_mat(h, [&](const auto& mat) {
+    dg::k_validate<<<dg::grid_for(32 * n_rows, 256), 256>>>(mat, h->d_row_ptr, n_rows, h->cols,
+                                                            h->d_bad);
     return cu(cudaGetLastError());
   });
   if (st) return fail(st);
   unsigned bad = 0;
   if ((st = cu(cudaMemcpy(&bad, h->d_bad, sizeof(unsigned), cudaMemcpyDeviceToHost)))) return fail(st);
   if (bad) return fail(DG_ERR_VALIDATION_FAILURE);
+  // --- (binary16, u16): one packed 32-bit stream, same 4 bytes per nonzero --------------------
+  const char* nopack = std::getenv("DG_NO_PACK");
+  if (h->value_precision == DG_HALF && h->index_bytes == 2 && !(nopack && *nopack == '1')) {
+    if ((st = cu(cudaMalloc(&h->d_packed, nz * 4)))) return fail(st);
+    dg::k_pack16<<<dg::grid_for(shard_nnz, 256), 256>>>(static_cast<const uint16_t*>(h->d_col),
+                                                        static_cast<const uint16_t*>(h->d_val),
+                                                        h->d_packed, shard_nnz);
+    if ((st = cu(cudaDeviceSynchronize()))) return fail(st);
+    cudaFree(h->d_col);
+    cudaFree(h->d_val);
+    h->d_col = h->d_val = nullptr;
+    h->packed = true;
+  }
+  h->matrix_bytes = (n_rows + 1) * 8 + shard_nnz * (h->value_bytes + h->index_bytes);
   if ((st = dg::finish_create(h, lens))) return fail(st);
   *out = reinterpret_cast<dg_handle*>(h);
   return DG_OK;
@@ -430,17 +426,18 @@ int dg_destroy(dg_handle* hh) {
   cudaFree(h->d_row_ptr);
   cudaFree(h->d_col);
   cudaFree(h->d_val);
+  cudaFree(h->d_packed);
   cudaFree(h->d_x);
   cudaFree(h->d_xf);
   cudaFree(h->d_y);
   cudaFree(h->d_bad);
+  for (auto* b : h->d_bin) cudaFree(b);
   for (uint32_t w = 0; w < Handle::kMaxWaves; ++w) {
     cudaFree(h->d_tiles[w]);
     cudaFree(h->d_segs[w]);
   }
   cudaFree(h->d_state);
   cudaFree(h->d_counters);
-  for (auto* b : h->d_bin) cudaFree(b);
   for (auto e : h->ev)
     if (e) cudaEventDestroy(e);
   for (auto e : h->kev)
@@ -514,32 +511,6 @@ int dg_last_timing(const dg_handle* hh, dg_timing* t) {
   return DG_OK;
 }
 
-int dg_copy_rows(const dg_handle* hh, uint64_t r0, uint64_t r1, uint64_t* rp_out,
-                 uint32_t* col_out, void* val_out) {
-  const Handle* h = reinterpret_cast<const Handle*>(hh);
-  if (!h || r0 > r1 || r1 > h->rows) return DG_ERR_INVALID_CONFIG;
-  DG_CUDA(cudaSetDevice(h->device));
-  DG_CUDA(cudaMemcpy(rp_out, h->d_row_ptr + r0, (r1 - r0 + 1) * 8, cudaMemcpyDeviceToHost));
-  const uint64_t b = rp_out[0], n = rp_out[r1 - r0] - b;
-  for (uint64_t i = 0; i <= r1 - r0; ++i) rp_out[i] -= b;
-  if (!n) return DG_OK;
-  DG_CUDA(cudaMemcpy(val_out, static_cast<const char*>(h->d_val) + b * h->value_bytes,
-                     n * h->value_bytes, cudaMemcpyDeviceToHost));
-  if (h->index_bytes == 4) {
-    DG_CUDA(cudaMemcpy(col_out, static_cast<const uint32_t*>(h->d_col) + b, n * 4,
-                       cudaMemcpyDeviceToHost));
-  } else {
-    uint32_t* wide = nullptr;
-    DG_CUDA(cudaMalloc(&wide, n * 4));
-    dg::k_widen_u16_u32<<<dg::grid_for(n, 256), 256>>>(static_cast<const uint16_t*>(h->d_col) + b,
-                                                       wide, n);
-    cudaError_t e = cudaMemcpy(col_out, wide, n * 4, cudaMemcpyDeviceToHost);
-    cudaFree(wide);
-    DG_CUDA(e);
-  }
-  return DG_OK;
-}
-
 int dg_kernel_times(const dg_handle* hh, dg_kernel_time* out, uint32_t cap, uint32_t* n_out) {
   Handle* h = const_cast<Handle*>(reinterpret_cast<const Handle*>(hh));
   if (!h || !n_out) return DG_ERR_INVALID_CONFIG;
@@ -568,6 +539,35 @@ int dg_copy_row_ptr(const dg_handle* hh, uint64_t r0, uint64_t r1, uint64_t* rp_
   if (!h || !rp_out || r0 > r1 || r1 > h->rows) return DG_ERR_INVALID_CONFIG;
   DG_CUDA(cudaSetDevice(h->device));
   DG_CUDA(cudaMemcpy(rp_out, h->d_row_ptr + r0, (r1 - r0 + 1) * 8, cudaMemcpyDeviceToHost));
+  return DG_OK;
+}
+
+int dg_copy_rows(const dg_handle* hh, uint64_t r0, uint64_t r1, uint64_t* rp_out,
+                 uint32_t* col_out, void* val_out) {
+  const Handle* h = reinterpret_cast<const Handle*>(hh);
+  if (!h || r0 > r1 || r1 > h->rows) return DG_ERR_INVALID_CONFIG;
+  DG_CUDA(cudaSetDevice(h->device));
+  DG_CUDA(cudaMemcpy(rp_out, h->d_row_ptr + r0, (r1 - r0 + 1) * 8, cudaMemcpyDeviceToHost));
+  const uint64_t b = rp_out[0], n = rp_out[r1 - r0] - b;
+  for (uint64_t i = 0; i <= r1 - r0; ++i) rp_out[i] -= b;
+  if (!n) return DG_OK;
+  uint32_t* d_col = nullptr;
+  void* d_val = nullptr;
+  DG_CUDA(cudaMalloc(&d_col, n * 4));
+  cudaError_t e = cudaMalloc(&d_val, n * h->value_bytes);
+  if (e == cudaSuccess) {
+    dg::dispatch_mat(h, [&](const auto& mat) {
+      using M = std::decay_t<decltype(mat)>;
+      dg::k_unpack<M><<<dg::grid_for(n, 256), 256>>>(mat, b, n, d_col,
+                                                     static_cast<typename M::Val*>(d_val));
+      return 0;
+    });
+    e = cudaMemcpy(col_out, d_col, n * 4, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(val_out, d_val, n * h->value_bytes, cudaMemcpyDeviceToHost);
+  }
+  cudaFree(d_col);
+  cudaFree(d_val);
+  DG_CUDA(e);
   return DG_OK;
 }
 

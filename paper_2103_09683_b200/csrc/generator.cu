@@ -19,6 +19,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <new>
 #include <vector>
 
@@ -119,10 +120,11 @@ __global__ void k_gen_lengths(Beams beams, uint64_t row0, uint64_t n_rows, uint6
   if (out64 && blockIdx.x == 0 && threadIdx.x == 0) out64[n_rows] = 0;
 }
 
+// Writes SoA (col, val) or, when packed != nullptr, Packed16 words (u16 columns only).
 template <typename I>
 __global__ void k_gen_fill(Beams beams, uint64_t row0, uint64_t n_rows,
                            const uint64_t* __restrict__ rp, I* __restrict__ col,
-                           uint16_t* __restrict__ val) {
+                           uint16_t* __restrict__ val, uint32_t* __restrict__ packed) {
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n_rows;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     uint64_t pos = rp[i];
@@ -134,9 +136,15 @@ __global__ void k_gen_fill(Beams beams, uint64_t row0, uint64_t n_rows,
       for (uint64_t t = 0; need > 0; ++t) {
         // Algorithm S: keep position t with probability need / (span - t).
         if (rng.next_double53() * static_cast<double>(d.span - t) < static_cast<double>(need)) {
-          col[pos] = static_cast<I>(b.col_offset + d.lo + t);
+          const uint64_t c = b.col_offset + d.lo + t;
           const double v = 0x1p-14 + (1.0 - 0x1p-14) * rng.next_double53();
-          val[pos] = __half_as_ushort(__double2half(v));
+          const uint16_t hv = __half_as_ushort(__double2half(v));
+          if (packed) {
+            packed[pos] = pack16(static_cast<uint16_t>(c), hv);
+          } else {
+            col[pos] = static_cast<I>(c);
+            val[pos] = hv;
+          }
           ++pos;
           --need;
         }
@@ -241,14 +249,24 @@ int dg_create_generated(const dg_profile* p, uint32_t n_beams, uint32_t index_by
   if ((st = cu(cudaMemcpy(rp.data(), h->d_row_ptr, (n + 1) * 8, cudaMemcpyDeviceToHost)))) return fail(st);
   h->nnz = rp[n];
   const uint64_t nz = std::max<uint64_t>(h->nnz, 1);
-  if ((st = cu(cudaMalloc(&h->d_val, nz * 2)))) return fail(st);
-  if ((st = cu(cudaMalloc(&h->d_col, nz * index_bytes)))) return fail(st);
-  if (index_bytes == 2)
-    dg::k_gen_fill<uint16_t><<<dg::grid_for(n, 128), 128>>>(
-        beams, r0, n, h->d_row_ptr, static_cast<uint16_t*>(h->d_col), static_cast<uint16_t*>(h->d_val));
-  else
-    dg::k_gen_fill<uint32_t><<<dg::grid_for(n, 128), 128>>>(
-        beams, r0, n, h->d_row_ptr, static_cast<uint32_t*>(h->d_col), static_cast<uint16_t*>(h->d_val));
+  const char* nopack = std::getenv("DG_NO_PACK");
+  if (index_bytes == 2 && !(nopack && *nopack == '1')) {  // (binary16, u16): Packed16 stream
+    if ((st = cu(cudaMalloc(&h->d_packed, nz * 4)))) return fail(st);
+    h->packed = true;
+    dg::k_gen_fill<uint16_t><<<dg::grid_for(n, 128), 128>>>(beams, r0, n, h->d_row_ptr, nullptr,
+                                                           nullptr, h->d_packed);
+  } else {
+    if ((st = cu(cudaMalloc(&h->d_val, nz * 2)))) return fail(st);
+    if ((st = cu(cudaMalloc(&h->d_col, nz * index_bytes)))) return fail(st);
+    if (index_bytes == 2)
+      dg::k_gen_fill<uint16_t><<<dg::grid_for(n, 128), 128>>>(
+          beams, r0, n, h->d_row_ptr, static_cast<uint16_t*>(h->d_col),
+          static_cast<uint16_t*>(h->d_val), nullptr);
+    else
+      dg::k_gen_fill<uint32_t><<<dg::grid_for(n, 128), 128>>>(
+          beams, r0, n, h->d_row_ptr, static_cast<uint32_t*>(h->d_col),
+          static_cast<uint16_t*>(h->d_val), nullptr);
+  }
   if ((st = cu(cudaGetLastError()))) return fail(st);
   if ((st = cu(cudaDeviceSynchronize()))) return fail(st);
   h->matrix_bytes = (n + 1) * 8 + h->nnz * (2 + index_bytes);

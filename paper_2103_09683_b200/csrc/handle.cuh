@@ -6,15 +6,17 @@
 
 #include <vector>
 
+#include "common.cuh"
 #include "dosegpu.h"
 
 namespace dg {
 
 constexpr int kNumBins = 8;
-constexpr int kBinLong = 6;     // L = 32: rows with len > 32, warp per row
+constexpr int kBinLong = 6;     // v0 plan (DG_PLAN=warp): rows with len > 32, warp per row
 constexpr int kBinGeneral = 7;  // L != 32: every non-empty row
-// Shared memory per tile CTA for the x window (2 CTAs per SM): 13,824 doubles / 27,648 floats.
-constexpr uint32_t kTileSmemBytes = 108 * 1024;
+// Shared memory of the tile CTA (one per SM): two x-window buffers of 110,592 bytes each,
+// i.e. 13,824 doubles (exact) or 27,648 floats (fp32) per window.
+constexpr uint32_t kWindowBytes = 108 * 1024;
 
 struct Handle {
   int device = 0;
@@ -23,22 +25,27 @@ struct Handle {
   uint32_t value_precision = DG_HALF, value_bytes = 2, index_bytes = 2;
   uint32_t lane_width = 32, accumulation = DG_ACCUM_EXACT;
 
-  // native encoding, shard-local (row_ptr rebased to 0)
+  // native encoding, shard-local (row_ptr rebased to 0).  (binary16, u16) matrices are kept as
+  // one packed u32 stream (Packed16: column << 16 | value bits); everything else as SoA arrays.
   uint64_t* d_row_ptr = nullptr;
-  void* d_col = nullptr;  // u16 or u32
-  void* d_val = nullptr;  // binary16 bits / f32 / f64
+  void* d_col = nullptr;  // u16 or u32 (SoA)
+  void* d_val = nullptr;  // binary16 bits / f32 / f64 (SoA)
+  uint32_t* d_packed = nullptr;
+  bool packed = false;
   uint64_t matrix_bytes = 0;
 
   // row plan: short-row bins ...
   uint32_t* d_bin[kNumBins] = {};
   uint32_t bin_count[kNumBins] = {};
+  uint64_t bin_nnz[kNumBins] = {};
   uint64_t plan_bytes = 0, nonempty_rows = 0;
   // ... and column-windowed tiles of row segments, per wave (plan.cu, spmv_tiles.cuh)
   static constexpr uint32_t kMaxWaves = 32;
-  static constexpr int kTileWarps = 16;
-  uint32_t acc_bytes = 8;                 // shared-memory x element: 8 exact, 4 fp32
-  uint32_t window_cols = 0;               // x window capacity per tile (columns)
-  uint64_t tile_nnz = 256 * 1024;         // target nonzeros per tile
+  static constexpr int kTileWarps = 32;
+  static constexpr int kTileUnroll = 8;
+  uint32_t acc_bytes = 8;          // shared-memory x element: 8 exact, 4 fp32
+  uint32_t window_cols = 0;        // x window capacity per buffer (columns)
+  uint64_t tile_nnz = 256 * 1024;  // target nonzeros per tile
   uint32_t n_waves = 0;
   uint64_t n_split_rows = 0;
   uint32_t wave_tiles[kMaxWaves] = {};
@@ -49,6 +56,7 @@ struct Handle {
   uint32_t* d_counters = nullptr;
   int sm_count = 148;
   bool use_tiles = false;
+  bool tiles_attr = false;
 
   // staging for host x / y and the fp32 family
   double* d_x = nullptr;
@@ -62,8 +70,7 @@ struct Handle {
   uint32_t n_kernels = 0;
 
   // per-launch profiling (DG_PROFILE)
-  static constexpr int kMaxLaunches = 16;
-  uint64_t bin_nnz[kNumBins] = {};
+  static constexpr int kMaxLaunches = 48;
   cudaEvent_t kev[kMaxLaunches + 1] = {};
   struct Launch {
     const char* name;
@@ -103,7 +110,31 @@ struct Handle {
   }
 };
 
-// shared by dosegpu.cu and generator.cu
+// Call f with the handle's element stream (Packed16 or SoA<V, I>).
+template <typename F>
+int dispatch_mat(const Handle* h, F&& f) {
+  if (h->packed) return f(Packed16{h->d_packed});
+  const bool u16 = h->index_bytes == 2;
+  switch (h->value_precision) {
+    case DG_HALF:
+      return u16 ? f(SoA<uint16_t, uint16_t>{static_cast<const uint16_t*>(h->d_col),
+                                             static_cast<const uint16_t*>(h->d_val)})
+                 : f(SoA<uint16_t, uint32_t>{static_cast<const uint32_t*>(h->d_col),
+                                             static_cast<const uint16_t*>(h->d_val)});
+    case DG_SINGLE:
+      return u16 ? f(SoA<float, uint16_t>{static_cast<const uint16_t*>(h->d_col),
+                                          static_cast<const float*>(h->d_val)})
+                 : f(SoA<float, uint32_t>{static_cast<const uint32_t*>(h->d_col),
+                                          static_cast<const float*>(h->d_val)});
+    default:
+      return u16 ? f(SoA<double, uint16_t>{static_cast<const uint16_t*>(h->d_col),
+                                           static_cast<const double*>(h->d_val)})
+                 : f(SoA<double, uint32_t>{static_cast<const uint32_t*>(h->d_col),
+                                           static_cast<const double*>(h->d_val)});
+  }
+}
+
+// shared by dosegpu.cu, plan.cu and generator.cu
 int select_device(int32_t want, int* dev_out);
 int check_options(const dg_options* o);
 int finish_create(Handle* h, const std::vector<uint64_t>& lens);

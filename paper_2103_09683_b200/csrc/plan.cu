@@ -16,24 +16,25 @@
 
 #include "common.cuh"
 #include "handle.cuh"
+#include "spmv_kernels.cuh"
 #include "spmv_tiles.cuh"
 
 namespace dg {
 
 // first / last column of every row (0, 0 for empty rows)
-template <typename I>
-__global__ void k_row_extents(const uint64_t* __restrict__ rp, const I* __restrict__ col,
-                              uint64_t rows, uint2* __restrict__ ext) {
+template <class M>
+__global__ void k_row_extents(M mat, const uint64_t* __restrict__ rp, uint64_t rows,
+                              uint2* __restrict__ ext) {
   for (uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; r < rows;
        r += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t s = rp[r], e = rp[r + 1];
-    ext[r] = s == e ? make_uint2(0, 0) : make_uint2(col[s], col[e - 1]);
+    ext[r] = s == e ? make_uint2(0, 0) : make_uint2(mat.col_at(s), mat.col_at(e - 1));
   }
 }
 
 // Greedy cut of wide rows: a segment starting at column c ends before the first column >= c+Ws.
-template <typename I>
-__global__ void k_split_rows(const uint64_t* __restrict__ rp, const I* __restrict__ col,
+template <class M>
+__global__ void k_split_rows(M mat, const uint64_t* __restrict__ rp,
                              const uint32_t* __restrict__ rows, uint32_t n_rows,
                              const uint64_t* __restrict__ out_off, uint32_t ws,
                              uint64_t* __restrict__ pos, uint2* __restrict__ cext,
@@ -45,14 +46,14 @@ __global__ void k_split_rows(const uint64_t* __restrict__ rp, const I* __restric
     uint64_t o = out_off[i];
     uint32_t k = 0;
     while (p < e) {
-      const uint64_t c = col[p], lim = c + ws;
+      const uint64_t c = mat.col_at(p), lim = c + ws;
       uint64_t lo = p + 1, hi = e;  // first q in (p, e] with col[q] >= lim (or e)
       while (lo < hi) {
         const uint64_t mid = lo + (hi - lo) / 2;
-        if (static_cast<uint64_t>(col[mid]) >= lim) hi = mid; else lo = mid + 1;
+        if (static_cast<uint64_t>(mat.col_at(mid)) >= lim) hi = mid; else lo = mid + 1;
       }
       pos[o + k] = p;
-      cext[o + k] = make_uint2(static_cast<uint32_t>(c), static_cast<uint32_t>(col[lo - 1]));
+      cext[o + k] = make_uint2(static_cast<uint32_t>(c), static_cast<uint32_t>(mat.col_at(lo - 1)));
       ++k;
       p = lo;
     }
@@ -68,8 +69,8 @@ struct HostSeg {
   uint16_t lane0, flags;
 };
 
-template <typename I>
-int plan_tiles_typed(Handle* h, const std::vector<uint64_t>& lens) {
+template <class M>
+int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens) {
   const uint64_t rows = h->rows;
   const uint32_t align = 16u / h->acc_bytes;                  // elements per 16 B (TMA alignment)
   const uint32_t W = h->window_cols;                          // window capacity (columns)
@@ -82,8 +83,7 @@ int plan_tiles_typed(Handle* h, const std::vector<uint64_t>& lens) {
   if (rows) {
     uint2* d_ext = nullptr;
     DG_CUDA(cudaMalloc(&d_ext, rows * sizeof(uint2)));
-    k_row_extents<I><<<grid_for(rows, 256), 256>>>(h->d_row_ptr, static_cast<const I*>(h->d_col),
-                                                    rows, d_ext);
+    k_row_extents<M><<<grid_for(rows, 256), 256>>>(mat, h->d_row_ptr, rows, d_ext);
     cudaError_t e = cudaMemcpy(ext.data(), d_ext, rows * sizeof(uint2), cudaMemcpyDeviceToHost);
     cudaFree(d_ext);
     DG_CUDA(e);
@@ -126,8 +126,8 @@ int plan_tiles_typed(Handle* h, const std::vector<uint64_t>& lens) {
     if (st == DG_OK) {
       cu(cudaMemcpy(d_rows, wide.data(), wide.size() * 4, cudaMemcpyHostToDevice));
       cu(cudaMemcpy(d_off, off.data(), (wide.size() + 1) * 8, cudaMemcpyHostToDevice));
-      k_split_rows<I><<<grid_for(wide.size(), 128), 128>>>(
-          h->d_row_ptr, static_cast<const I*>(h->d_col), d_rows, static_cast<uint32_t>(wide.size()),
+      k_split_rows<M><<<grid_for(wide.size(), 128), 128>>>(
+          mat, h->d_row_ptr, d_rows, static_cast<uint32_t>(wide.size()),
           d_off, ws, d_pos, d_cext, d_cnt);
       cu(cudaGetLastError());
       cu(cudaMemcpy(pos.data(), d_pos, total * 8, cudaMemcpyDeviceToHost));
@@ -215,8 +215,7 @@ int plan_tiles_typed(Handle* h, const std::vector<uint64_t>& lens) {
 }  // namespace
 
 int plan_tiles(Handle* h, const std::vector<uint64_t>& lens) {
-  return h->index_bytes == 2 ? plan_tiles_typed<uint16_t>(h, lens)
-                             : plan_tiles_typed<uint32_t>(h, lens);
+  return dispatch_mat(h, [&](const auto& mat) { return plan_tiles_typed(h, mat, lens); });
 }
 
 }  // namespace dg

@@ -3,8 +3,15 @@
 // Why: the dose gather x[col[j]] is the dominant L1 cost of a lane-strided CSR SpMV (32 lanes of
 // a sparse row touch ~16 sectors of x per request; v0 ncu: 6.5 sectors/request, 42% of HBM).  The
 // row plan (plan.cu) sorts row segments by first column and cuts them into tiles whose column
-// window [xlo, xlo + xlen) fits in shared memory; one CTA stages the tile's window with
-// cp.async.bulk (UBLKCP) and its warps gather x from shared memory instead of L1/L2.
+// window [xlo, xlo + xlen) fits in shared memory; the CTA stages windows with cp.async.bulk
+// (SASS UBLKCP) into a 2-buffer ring, and its warps gather x with LDS instead of L1/L2 loads.
+//
+// Pipeline (one CTA of WARPS warps per SM, no CTA-wide barrier in the steady state):
+//   buffer b holds tile tile_of[b]; warps pull its segments with a shared-memory counter; the last
+//   warp to leave buffer b claims the next tile from the global counter and re-arms b (TMA +
+//   mbarrier expect_tx) while the other warps already work on buffer b^1.
+// Inside a segment each lane software-pipelines its matrix loads: batch k+1 (U positions per
+// lane) is in flight while batch k is gathered and accumulated.
 //
 // Exactness: a segment is a contiguous position range [p0, p0 + n) of one row; physical lane l
 // owns the row's logical lane l (positions j with (j - row_start) % 32 == l), accumulates them in
@@ -15,6 +22,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "spmv_kernels.cuh"
 
 namespace dg {
 
@@ -29,7 +37,7 @@ struct Segment {  // 24 bytes
 constexpr uint16_t kSegFirst = 1, kSegLast = 2;
 
 struct Tile {  // 16 bytes
-  uint32_t xlo, xlen;  // x window (xlo even, xlen even)
+  uint32_t xlo, xlen;  // x window (16-byte aligned start, 16-byte multiple length)
   uint32_t seg0, seg1;
 };
 
@@ -43,6 +51,9 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -63,100 +74,134 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       : "memory");
 }
 
-template <typename Acc>
-struct AccOps;
-template <>
-struct AccOps<double> {
-  template <typename V>
-  __device__ static __forceinline__ double prod(V v, double xv) { return __dmul_rn(widen(v), xv); }
-  __device__ static __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
-};
-template <>
-struct AccOps<float> {
-  template <typename V>
-  __device__ static __forceinline__ float prod(V v, float xv) { return __fmul_rn(widen_f(v), xv); }
-  __device__ static __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
-};
-
-// Persistent: CTAs pull tiles from *counter in plan order; warps pull the tile's segments.
-template <typename V, typename I, typename Acc, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, 2)
-    k_tiles(const I* __restrict__ col, const V* __restrict__ val, const Acc* __restrict__ x,
-            const Tile* __restrict__ tiles, uint32_t n_tiles, const Segment* __restrict__ segs,
-            Acc* __restrict__ state, double* __restrict__ y, uint32_t* __restrict__ counter) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  Acc* xs = reinterpret_cast<Acc*>(smem_raw);
-  __shared__ __align__(8) uint64_t bar;
-  __shared__ uint32_t s_tile, s_next;
+// One segment on one warp (see the header comment for the lane/position contract).
+template <int U, class M, typename Acc>
+__device__ __forceinline__ void run_segment(const M& mat, const Acc* __restrict__ xs,
+                                            uint32_t xlo, const Segment& S,
+                                            Acc* __restrict__ state, double* __restrict__ y,
+                                            uint32_t lane) {
   using Ops = AccOps<Acc>;
+  using Raw = typename M::Raw;
+  const uint64_t p0 = S.p0, p1 = S.p0 + S.n;
+  Acc acc = (S.flags & kSegFirst) ? Acc(0) : state[static_cast<uint64_t>(S.slot) * 32 + lane];
+  uint64_t base = p0 - S.lane0;
+  {  // head chunk: positions before p0 belong to the row's previous segment
+    const uint64_t j = base + lane;
+    if (j >= p0 && j < p1) {
+      const Raw e = mat.load(j);
+      acc = Ops::add(acc, Ops::prod(M::v_of(e), xs[M::c_of(e) - xlo]));
+    }
+    base += 32;
+  }
+  const uint64_t nb = base < p1 ? (p1 - base) / (32 * U) : 0;
+  Raw ra[U], rb[U];
+  auto load = [&](Raw* r, uint64_t b) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) r[u] = mat.load(b + lane + 32 * u);
+  };
+  auto consume = [&](const Raw* r) {
+    Acc xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = xs[M::c_of(r[u]) - xlo];
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc = Ops::add(acc, Ops::prod(M::v_of(r[u]), xv[u]));
+  };
+  if (nb) load(ra, base);
+  for (uint64_t k = 0; k < nb; k += 2) {  // ping-pong: the next batch is in flight during consume
+    if (k + 1 < nb) load(rb, base + 32 * U);
+    consume(ra);
+    base += 32 * U;
+    if (k + 1 >= nb) break;
+    if (k + 2 < nb) load(ra, base + 32 * U);
+    consume(rb);
+    base += 32 * U;
+  }
+  for (; base < p1; base += 32) {
+    const uint64_t j = base + lane;
+    if (j < p1) {
+      const Raw e = mat.load(j);
+      acc = Ops::add(acc, Ops::prod(M::v_of(e), xs[M::c_of(e) - xlo]));
+    }
+  }
+  if (S.flags & kSegLast) {
+#pragma unroll
+    for (int off = 16; off >= 1; off /= 2) acc = Ops::add(acc, __shfl_down_sync(kFull, acc, off));
+    if (lane == 0) y[S.row] = static_cast<double>(acc);
+  } else {
+    state[static_cast<uint64_t>(S.slot) * 32 + lane] = acc;
+  }
+}
+
+// Persistent: one CTA per SM; dynamic smem = 2 * wcap * sizeof(Acc) (two x-window buffers).
+template <class M, typename Acc, int WARPS, int U>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+    k_tiles(M mat, const Acc* __restrict__ x, const Tile* __restrict__ tiles, uint32_t n_tiles,
+            const Segment* __restrict__ segs, Acc* __restrict__ state, double* __restrict__ y,
+            uint32_t* __restrict__ counter, uint32_t wcap) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[2];
+  __shared__ uint32_t tile_of[2], seg_next[2], done[2];
+  Acc* const xbuf0 = reinterpret_cast<Acc*>(smem_raw);
   const uint32_t lane = threadIdx.x & 31;
+
+  // claim the next tile for buffer b and start its window transfer (one thread)
+  auto refill = [&](int b) {
+    const uint32_t t = atomicAdd(counter, 1u);
+    tile_of[b] = t;
+    seg_next[b] = 0;
+    done[b] = 0;
+    if (t < n_tiles) {
+      const Tile T = tiles[t];
+      // order earlier generic-proxy reads of this buffer before the async-proxy overwrite
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const uint32_t bytes = T.xlen * static_cast<uint32_t>(sizeof(Acc));
+      mbar_arrive_expect_tx(&full[b], bytes);
+      const char* src = reinterpret_cast<const char*>(x + T.xlo);
+      char* dst = reinterpret_cast<char*>(xbuf0 + b * wcap);
+      for (uint32_t off = 0; off < bytes; off += 32768u)
+        tma_load_1d(dst + off, src + off, min(32768u, bytes - off), &full[b]);
+    } else {
+      mbar_arrive(&full[b]);  // terminal: completes the phase with tile_of[b] >= n_tiles
+    }
+  };
+
   if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    refill(0);
+    refill(1);
   }
   __syncthreads();
-  uint32_t phase = 0;
+
+  uint32_t phase0 = 0, phase1 = 0;
+  int b = 0;
   for (;;) {
-    if (threadIdx.x == 0) {
-      s_tile = atomicAdd(counter, 1u);
-      s_next = 0;
-    }
-    __syncthreads();
-    const uint32_t t = s_tile;
+    if (b == 0) { mbar_wait(&full[0], phase0); phase0 ^= 1u; }
+    else        { mbar_wait(&full[1], phase1); phase1 ^= 1u; }
+    const uint32_t t = *reinterpret_cast<volatile uint32_t*>(&tile_of[b]);
     if (t >= n_tiles) break;
     const Tile T = tiles[t];
-    if (threadIdx.x == 0) {
-      // order this CTA's earlier generic-proxy reads of xs before the async-proxy overwrite
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      const uint32_t bytes = (T.xlen * sizeof(Acc) + 15u) & ~15u;
-      mbar_arrive_expect_tx(&bar, bytes);
-      const char* src = reinterpret_cast<const char*>(x + T.xlo);
-      for (uint32_t off = 0; off < bytes; off += 32768u)
-        tma_load_1d(reinterpret_cast<char*>(xs) + off, src + off, min(32768u, bytes - off), &bar);
-    }
-    mbar_wait(&bar, phase);
-    phase ^= 1u;
-    const uint32_t xlo = T.xlo;  // xs[c - xlo] == x[c] for c in the window
+    const Acc* xs = xbuf0 + b * wcap;
     const uint32_t nseg = T.seg1 - T.seg0;
     for (;;) {
       uint32_t k = 0;
-      if (lane == 0) k = atomicAdd(&s_next, 1u);
+      if (lane == 0) k = atomicAdd(&seg_next[b], 1u);
       k = __shfl_sync(kFull, k, 0);
       if (k >= nseg) break;
       const Segment S = segs[T.seg0 + k];
-      const uint64_t p0 = S.p0, p1 = S.p0 + S.n;
-      Acc acc = (S.flags & kSegFirst) ? Acc(0) : state[static_cast<uint64_t>(S.slot) * 32 + lane];
-      uint64_t base = p0 - S.lane0;
-      {  // head chunk (positions before p0 belong to the previous segment)
-        const uint64_t j = base + lane;
-        if (j >= p0 && j < p1) acc = Ops::add(acc, Ops::prod(ld_stream(val + j), xs[ld_stream(col + j) - xlo]));
-        base += 32;
-      }
-      constexpr int U = 8;
-      for (; base + 32 * U <= p1; base += 32 * U) {
-        I c[U];
-        V v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          c[u] = ld_stream(col + base + lane + 32 * u);
-          v[u] = ld_stream(val + base + lane + 32 * u);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) acc = Ops::add(acc, Ops::prod(v[u], xs[c[u] - xlo]));
-      }
-      for (; base < p1; base += 32) {
-        const uint64_t j = base + lane;
-        if (j < p1) acc = Ops::add(acc, Ops::prod(ld_stream(val + j), xs[ld_stream(col + j) - xlo]));
-      }
-      if (S.flags & kSegLast) {
-#pragma unroll
-        for (int off = 16; off >= 1; off /= 2) acc = Ops::add(acc, __shfl_down_sync(kFull, acc, off));
-        if (lane == 0) y[S.row] = static_cast<double>(acc);
-      } else {
-        state[static_cast<uint64_t>(S.slot) * 32 + lane] = acc;
+      run_segment<U>(mat, xs, T.xlo, S, state, y, lane);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();  // this warp's reads of buffer b happen before the count
+      if (atomicAdd(&done[b], 1u) == WARPS - 1) {
+        __threadfence_block();
+        refill(b);
       }
     }
-    __syncthreads();  // every warp is done with xs before the next tile's TMA
+    __syncwarp();
+    b ^= 1;
   }
 }
 
