@@ -121,13 +121,22 @@ int check_options(const dg_options* o) {
 // DG_PLAN=warp keeps the v0 warp-per-row bin instead, longest row first.
 int build_plan(Handle* h, const std::vector<uint64_t>& lens) {
   std::vector<std::vector<uint32_t>> bins(kNumBins);
-  uint64_t nonempty = 0;
+  uint64_t nonempty = 0, short_rows = 0;
+  for (uint64_t len : lens) {
+    nonempty += len > 0;
+    short_rows += len > 0 && len <= 32;
+  }
+  // Few short rows: fold them into the tiles (a warp per row, one fewer launch per bin); many:
+  // sub-warp bins, G = next_pow2(len) lanes per row.
+  h->short_max = short_rows * 20 < nonempty ? 0 : 32;
+  if (const char* sm = std::getenv("DG_SHORT_MAX"))
+    h->short_max = std::min<uint64_t>(32, std::strtoull(sm, nullptr, 10));
   for (uint64_t r = 0; r < lens.size(); ++r) {
     const uint64_t len = lens[r];
     if (len == 0) continue;
-    ++nonempty;
     int b;
     if (h->lane_width != 32) b = kBinGeneral;
+    else if (h->use_tiles && len > h->short_max) continue;  // plan_tiles owns it
     else if (len == 1) b = 0;
     else if (len == 2) b = 1;
     else if (len <= 4) b = 2;

@@ -47,7 +47,8 @@ struct Handle {
   uint32_t window_cols = 0;        // x window capacity per buffer (columns)
   uint64_t tile_nnz = 256 * 1024;  // target nonzeros per tile
   uint32_t n_waves = 0;
-  uint64_t n_split_rows = 0;
+  uint64_t n_split_rows = 0, n_global_rows = 0;
+  uint64_t short_max = 32;  // rows with len <= short_max use the sub-warp bins, others the tiles
   uint32_t wave_tiles[kMaxWaves] = {};
   uint64_t wave_nnz[kMaxWaves] = {}, wave_rows[kMaxWaves] = {};
   void* d_tiles[kMaxWaves] = {};

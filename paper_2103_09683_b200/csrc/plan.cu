@@ -89,15 +89,24 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     DG_CUDA(e);
   }
 
-  // 2. segments: one per narrow long row, greedy cuts for wide rows
+  // 2. segments: one per row that fits a window; a dense row wider than a window stays whole and
+  //    reads x from global (its lanes read consecutive x: 2 sectors per 32 positions); a sparse
+  //    wide row (e.g. a multi-beam row of C4) is cut greedily into windowed segments, one wave
+  //    per segment, carrying its 32 lane partials between waves
   std::vector<std::vector<HostSeg>> waves(1);
+  std::vector<HostSeg> global_x;
   std::vector<uint32_t> wide;
   for (uint64_t r = 0; r < rows; ++r) {
-    if (lens[r] <= 32) continue;
+    if (lens[r] == 0 || lens[r] <= h->short_max) continue;
     const uint32_t c0 = ext[r].x, c1 = ext[r].y;
-    if (static_cast<uint64_t>(c1) - c0 + 1 <= ws) {
+    const uint64_t span = static_cast<uint64_t>(c1) - c0 + 1;
+    const uint16_t whole = static_cast<uint16_t>(kSegFirst | kSegLast);
+    if (span <= ws) {
       waves[0].push_back({rp[r], static_cast<uint32_t>(lens[r]), static_cast<uint32_t>(r), 0, c0,
-                          c1, 0, static_cast<uint16_t>(kSegFirst | kSegLast)});
+                          c1, 0, whole});
+    } else if (4 * lens[r] >= 3 * span) {
+      global_x.push_back({rp[r], static_cast<uint32_t>(lens[r]), static_cast<uint32_t>(r), 0, c0,
+                          c1, 0, static_cast<uint16_t>(whole | kSegGlobalX)});
     } else {
       wide.push_back(static_cast<uint32_t>(r));
     }
@@ -153,8 +162,9 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
 
   // 3. tiles per wave
   const uint64_t xcap = (h->cols + align - 1) / align * align;  // padded x length on device
-  h->n_waves = static_cast<uint32_t>(std::min<size_t>(waves.size(), Handle::kMaxWaves));
   if (waves.size() > Handle::kMaxWaves) return DG_ERR_UNSUPPORTED_FEATURE;
+  h->n_waves = static_cast<uint32_t>(waves.size());
+  h->n_global_rows = global_x.size();
   for (uint32_t w = 0; w < h->n_waves; ++w) {
     auto& S = waves[w];
     std::stable_sort(S.begin(), S.end(), [](const HostSeg& a, const HostSeg& b) {
@@ -162,8 +172,26 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     });
     std::vector<Tile> tiles;
     std::vector<Segment> segs;
-    segs.reserve(S.size());
+    segs.reserve(S.size() + (w == 0 ? global_x.size() : 0));
     uint64_t wave_nnz = 0, wave_rows = 0;
+    if (w == 0 && !global_x.empty()) {
+      // global-x tiles first (no window), longest rows first: they are the longest work items
+      std::stable_sort(global_x.begin(), global_x.end(),
+                       [](const HostSeg& a, const HostSeg& b) { return a.n > b.n; });
+      size_t g = 0;
+      while (g < global_x.size()) {
+        uint64_t nnz = 0;
+        const uint32_t s0 = static_cast<uint32_t>(segs.size());
+        while (g < global_x.size() && (nnz == 0 || nnz + global_x[g].n <= h->tile_nnz)) {
+          const HostSeg& q = global_x[g++];
+          segs.push_back({q.p0, q.n, q.row, 0, 0, q.flags});
+          nnz += q.n;
+          wave_nnz += q.n;
+          ++wave_rows;
+        }
+        tiles.push_back({0, 0, s0, static_cast<uint32_t>(segs.size())});
+      }
+    }
     size_t i = 0;
     while (i < S.size()) {
       const uint32_t xlo = S[i].clo / align * align;

@@ -34,7 +34,7 @@ struct Segment {  // 24 bytes
   uint16_t lane0;  // (p0 - row_start) % 32
   uint16_t flags;  // kSegFirst | kSegLast
 };
-constexpr uint16_t kSegFirst = 1, kSegLast = 2;
+constexpr uint16_t kSegFirst = 1, kSegLast = 2, kSegGlobalX = 4;
 
 struct Tile {  // 16 bytes
   uint32_t xlo, xlen;  // x window (16-byte aligned start, 16-byte multiple length)
@@ -74,27 +74,39 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       : "memory");
 }
 
+// x sources: the tile's shared-memory window, or global x (L1/L2) for dense wide rows whose
+// column span exceeds a window (kSegGlobalX) -- their 32 lanes read 32 consecutive x entries.
+template <typename Acc>
+struct XWindow {
+  const Acc* xs;
+  uint32_t xlo;
+  __device__ __forceinline__ Acc operator()(uint32_t c) const { return xs[c - xlo]; }
+};
+template <typename Acc>
+struct XGlobal {
+  const Acc* x;
+  __device__ __forceinline__ Acc operator()(uint32_t c) const { return __ldg(x + c); }
+};
+
 // One segment on one warp (see the header comment for the lane/position contract).
-template <int U, class M, typename Acc>
-__device__ __forceinline__ void run_segment(const M& mat, const Acc* __restrict__ xs,
-                                            uint32_t xlo, const Segment& S,
+template <int U, class M, typename Acc, class X>
+__device__ __forceinline__ void run_segment(const M& mat, const X& xr, const Segment& S,
                                             Acc* __restrict__ state, double* __restrict__ y,
                                             uint32_t lane) {
   using Ops = AccOps<Acc>;
   using Raw = typename M::Raw;
   const uint64_t p0 = S.p0, p1 = S.p0 + S.n;
-  Acc acc = (S.flags & kSegFirst) ? Acc(0) : state[static_cast<uint64_t>(S.slot) * 32 + lane];
   uint64_t base = p0 - S.lane0;
-  {  // head chunk: positions before p0 belong to the row's previous segment
-    const uint64_t j = base + lane;
-    if (j >= p0 && j < p1) {
-      const Raw e = mat.load(j);
-      acc = Ops::add(acc, Ops::prod(M::v_of(e), xs[M::c_of(e) - xlo]));
-    }
-    base += 32;
-  }
+  // head chunk (positions before p0 belong to the row's previous segment) and the first full
+  // batch are issued together, before anything is consumed
+  const uint64_t jh = base + lane;
+  const bool head = jh >= p0 && jh < p1;
+  Raw rh{};
+  if (head) rh = mat.load(jh);
+  base += 32;
   const uint64_t nb = base < p1 ? (p1 - base) / (32 * U) : 0;
   Raw ra[U], rb[U];
+  Acc acc;
   auto load = [&](Raw* r, uint64_t b) {
 #pragma unroll
     for (int u = 0; u < U; ++u) r[u] = mat.load(b + lane + 32 * u);
@@ -102,11 +114,13 @@ __device__ __forceinline__ void run_segment(const M& mat, const Acc* __restrict_
   auto consume = [&](const Raw* r) {
     Acc xv[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) xv[u] = xs[M::c_of(r[u]) - xlo];
+    for (int u = 0; u < U; ++u) xv[u] = xr(M::c_of(r[u]));
 #pragma unroll
     for (int u = 0; u < U; ++u) acc = Ops::add(acc, Ops::prod(M::v_of(r[u]), xv[u]));
   };
   if (nb) load(ra, base);
+  acc = (S.flags & kSegFirst) ? Acc(0) : state[static_cast<uint64_t>(S.slot) * 32 + lane];
+  if (head) acc = Ops::add(acc, Ops::prod(M::v_of(rh), xr(M::c_of(rh))));
   for (uint64_t k = 0; k < nb; k += 2) {  // ping-pong: the next batch is in flight during consume
     if (k + 1 < nb) load(rb, base + 32 * U);
     consume(ra);
@@ -120,7 +134,7 @@ __device__ __forceinline__ void run_segment(const M& mat, const Acc* __restrict_
     const uint64_t j = base + lane;
     if (j < p1) {
       const Raw e = mat.load(j);
-      acc = Ops::add(acc, Ops::prod(M::v_of(e), xs[M::c_of(e) - xlo]));
+      acc = Ops::add(acc, Ops::prod(M::v_of(e), xr(M::c_of(e))));
     }
   }
   if (S.flags & kSegLast) {
@@ -154,7 +168,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       const Tile T = tiles[t];
       // order earlier generic-proxy reads of this buffer before the async-proxy overwrite
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      const uint32_t bytes = T.xlen * static_cast<uint32_t>(sizeof(Acc));
+      const uint32_t bytes = T.xlen * static_cast<uint32_t>(sizeof(Acc));  // 0: global-x tile
       mbar_arrive_expect_tx(&full[b], bytes);
       const char* src = reinterpret_cast<const char*>(x + T.xlo);
       char* dst = reinterpret_cast<char*>(xbuf0 + b * wcap);
@@ -182,15 +196,28 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     const uint32_t t = *reinterpret_cast<volatile uint32_t*>(&tile_of[b]);
     if (t >= n_tiles) break;
     const Tile T = tiles[t];
-    const Acc* xs = xbuf0 + b * wcap;
+    const XWindow<Acc> xw{xbuf0 + b * wcap, T.xlo};
+    const XGlobal<Acc> xg{x};
     const uint32_t nseg = T.seg1 - T.seg0;
-    for (;;) {
+    auto grab = [&]() {
       uint32_t k = 0;
       if (lane == 0) k = atomicAdd(&seg_next[b], 1u);
-      k = __shfl_sync(kFull, k, 0);
-      if (k >= nseg) break;
-      const Segment S = segs[T.seg0 + k];
-      run_segment<U>(mat, xs, T.xlo, S, state, y, lane);
+      return __shfl_sync(kFull, k, 0);
+    };
+    // the next segment's descriptor is claimed and loaded while the current one streams
+    uint32_t k = grab();
+    Segment S{};
+    if (k < nseg) S = segs[T.seg0 + k];
+    while (k < nseg) {
+      const uint32_t k2 = grab();
+      Segment S2{};
+      if (k2 < nseg) S2 = segs[T.seg0 + k2];
+      if (S.flags & kSegGlobalX)
+        run_segment<U>(mat, xg, S, state, y, lane);
+      else
+        run_segment<U>(mat, xw, S, state, y, lane);
+      k = k2;
+      S = S2;
     }
     __syncwarp();
     if (lane == 0) {

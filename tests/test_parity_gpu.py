@@ -386,6 +386,8 @@ def _wide_row_matrix(port, rows=3000, cols=40_000, seed=5):
     lens = np.where(rng.random(rows) < 0.5, 0, rng.integers(1, 3000, rows))
     lens[rng.choice(rows, 40, replace=False)] = rng.integers(14_000, cols + 1, 40)  # wide, dense
     lens[:3] = [cols, 13_823, 27_647]
+    sparse_wide = rng.choice(np.arange(3, rows), 30, replace=False)  # wide but sparse: split
+    lens[sparse_wide] = rng.integers(40, 3000, 30)
     rp = np.zeros(rows + 1, dtype=np.uint64)
     np.cumsum(lens, out=rp[1:])
     col = np.empty(int(rp[-1]), dtype=np.uint32)
@@ -393,7 +395,9 @@ def _wide_row_matrix(port, rows=3000, cols=40_000, seed=5):
         n = int(lens[r])
         if n == 0:
             continue
-        if n >= 4096:
+        if r in sparse_wide:  # spread over up to the whole column range
+            c = np.sort(rng.choice(cols, n, replace=False))
+        elif n >= 4096:
             lo = int(rng.integers(0, cols - n + 1))
             c = np.arange(lo, lo + n)
         else:
@@ -412,8 +416,12 @@ def test_windowed_tiles_with_split_rows_bit_exact(port, monkeypatch, tile_nnz):
     want = port.spmv_rowchunk(m, x, 32, 4)
     with dg.DoseEngine.from_csr(to_dg(m)) as e:
         got = e.dose(x)
-        assert e.info["n_kernels"] >= 3  # short-row bins + >= 2 waves
+        assert e.info["n_kernels"] >= 2  # >= 2 waves (sparse wide rows are split)
     assert np.array_equal(bits(got), bits(want))
+    for short_max in ("0", "32"):  # short rows folded into tiles / in sub-warp bins
+        monkeypatch.setenv("DG_SHORT_MAX", short_max)
+        with dg.DoseEngine.from_csr(to_dg(m)) as e:
+            assert np.array_equal(bits(e.dose(x)), bits(want))
     with dg.DoseEngine.from_csr(to_dg(m), accumulation=dg.ACCUM_FP32) as e:
         gf = e.dose(x)
     assert np.max(np.abs(gf - want)) <= FP32_TOL * np.max(np.abs(want))
