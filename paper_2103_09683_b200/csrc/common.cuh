@@ -58,6 +58,8 @@ struct SoA {
   __device__ __forceinline__ Idx col_at(uint64_t j) const { return col[j]; }
   __device__ __forceinline__ static I c_of(const Raw& r) { return r.c; }
   __device__ __forceinline__ static V v_of(const Raw& r) { return r.v; }
+  // a placeholder element for masked-off lanes: a valid column, value bits 0
+  __device__ __forceinline__ static Raw filler(uint32_t col) { return {static_cast<I>(col), V(0)}; }
 };
 
 // Packed16: the native (binary16 value, u16 column) pair of one nonzero in one 32-bit word,
@@ -72,6 +74,7 @@ struct Packed16 {
   __device__ __forceinline__ Idx col_at(uint64_t j) const { return static_cast<uint16_t>(w[j] >> 16); }
   __device__ __forceinline__ static uint16_t c_of(Raw r) { return static_cast<uint16_t>(r >> 16); }
   __device__ __forceinline__ static uint16_t v_of(Raw r) { return static_cast<uint16_t>(r & 0xFFFFu); }
+  __device__ __forceinline__ static Raw filler(uint32_t col) { return col << 16; }
 };
 
 __device__ __forceinline__ uint32_t pack16(uint16_t col, uint16_t half_bits) {

@@ -174,13 +174,10 @@ void launch_group(Handle* h, int b, const char* name, cudaStream_t s, const M& m
 
 // One persistent launch per wave (one CTA per SM): wave k continues the segments whose lane
 // partials wave k-1 stored.
-template <class M, typename Acc>
-int launch_tiles(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t s,
-                 const char* name) {
-  if (!h->n_waves) return DG_OK;
-  constexpr int kWarps = Handle::kTileWarps, kU = Handle::kTileUnroll;
+template <class M, typename Acc, int kWarps, int kU>
+int launch_tiles_cfg(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t s) {
   const size_t smem = 2ull * h->window_cols * sizeof(Acc);
-  if (!h->tiles_attr) {  // a handle has one (M, Acc) and one device
+  if (!h->tiles_attr) {  // a handle has one (M, Acc, config) and one device
     DG_CUDA(cudaFuncSetAttribute(k_tiles<M, Acc, kWarps, kU>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
@@ -196,11 +193,28 @@ int launch_tiles(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t 
         mat, x, static_cast<const Tile*>(h->d_tiles[w]), h->wave_tiles[w],
         static_cast<const Segment*>(h->d_segs[w]), static_cast<Acc*>(h->d_state), y,
         h->d_counters + w, h->window_cols);
-    (void)name;
     h->post(s, kWaveName[std::min<uint32_t>(w, 8)], h->wave_rows[w], h->wave_nnz[w]);
   }
   DG_CUDA(cudaGetLastError());
   return DG_OK;
+}
+
+// (warps per CTA, batch depth U) of the tile kernel; DG_TILE_CFG selects an alternative for the
+// hot (Packed16) stream when measuring.
+template <class M, typename Acc>
+int launch_tiles(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t s,
+                 const char* /*name*/) {
+  if (!h->n_waves) return DG_OK;
+  if constexpr (std::is_same_v<M, Packed16>) {
+    switch (h->tile_cfg) {
+      case 1: return launch_tiles_cfg<M, Acc, 32, 4>(h, mat, x, y, s);
+      case 2: return launch_tiles_cfg<M, Acc, 32, 8>(h, mat, x, y, s);
+      case 3: return launch_tiles_cfg<M, Acc, 16, 16>(h, mat, x, y, s);
+      case 4: return launch_tiles_cfg<M, Acc, 32, 6>(h, mat, x, y, s);
+      default: break;
+    }
+  }
+  return launch_tiles_cfg<M, Acc, Handle::kTileWarps, Handle::kTileUnroll>(h, mat, x, y, s);
 }
 
 template <class M>
@@ -283,6 +297,7 @@ int finish_create(Handle* h, const std::vector<uint64_t>& lens) {
   h->acc_bytes = h->accumulation == DG_ACCUM_FP32 ? 4 : 8;
   h->window_cols = kWindowBytes / h->acc_bytes;
   if (const char* tn = std::getenv("DG_TILE_NNZ")) h->tile_nnz = std::strtoull(tn, nullptr, 10);
+  if (const char* tc = std::getenv("DG_TILE_CFG")) h->tile_cfg = std::atoi(tc);
   DG_TRY(build_plan(h, lens));
   if (h->use_tiles) DG_TRY(plan_tiles(h, lens));
   // x staging is padded to a 16-byte multiple: the 1-D TMA moves 16-byte granules

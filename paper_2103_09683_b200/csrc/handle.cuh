@@ -41,7 +41,7 @@ struct Handle {
   uint64_t plan_bytes = 0, nonempty_rows = 0;
   // ... and column-windowed tiles of row segments, per wave (plan.cu, spmv_tiles.cuh)
   static constexpr uint32_t kMaxWaves = 32;
-  static constexpr int kTileWarps = 32;
+  static constexpr int kTileWarps = 24;
   static constexpr int kTileUnroll = 8;
   uint32_t acc_bytes = 8;          // shared-memory x element: 8 exact, 4 fp32
   uint32_t window_cols = 0;        // x window capacity per buffer (columns)
@@ -58,6 +58,7 @@ struct Handle {
   int sm_count = 148;
   bool use_tiles = false;
   bool tiles_attr = false;
+  int tile_cfg = 0;  // DG_TILE_CFG: alternative (warps, U) configurations for A/B
 
   // staging for host x / y and the fp32 family
   double* d_x = nullptr;

@@ -88,61 +88,111 @@ struct XGlobal {
   __device__ __forceinline__ Acc operator()(uint32_t c) const { return __ldg(x + c); }
 };
 
-// One segment on one warp (see the header comment for the lane/position contract).
+// A segment as the warp's pipeline sees it: batches of U chunks of 32 positions aligned to the
+// row's lane grid (chunk c covers base0 + 32c + lane); positions outside [p0, p1) are masked.
+struct SegRun {
+  uint64_t base0;   // row-aligned start: positions base0 + rel, rel in [lo, hi) are the segment's
+  uint32_t lo, hi;  // lo = lane0, hi = lane0 + n
+  uint32_t nbatch, row, slot, flags;
+};
+template <int U>
+__device__ __forceinline__ SegRun seg_run(const Segment& S) {
+  SegRun r;
+  r.base0 = S.p0 - S.lane0;
+  r.lo = S.lane0;
+  r.hi = S.lane0 + S.n;
+  r.nbatch = ((r.hi + 31) / 32 + U - 1) / U;
+  r.row = S.row;
+  r.slot = S.slot;
+  r.flags = S.flags;
+  return r;
+}
+
+// Issue batch b of segment s: U predicated requests (one 128-B request per chunk for Packed16).
+// Masked-off lanes get a filler element whose column (`safe_col`, the tile's window start) is a
+// valid x index, so the gather below needs no predicate; only the accumulation is masked.
+template <int U, class M>
+__device__ __forceinline__ uint32_t load_batch(const M& mat, typename M::Raw* r, const SegRun& s,
+                                               uint32_t b, uint32_t lane, uint32_t safe_col) {
+  uint32_t mask = 0;
+  const uint32_t rel0 = b * (32 * U) + lane;
+  const uint64_t base = s.base0 + rel0;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint32_t rel = rel0 + 32 * u;
+    const bool ok = rel >= s.lo && rel < s.hi;
+    r[u] = ok ? mat.load(base + 32 * u) : M::filler(safe_col);
+    mask |= static_cast<uint32_t>(ok) << u;
+  }
+  return mask;
+}
+
+// Gather x for a loaded batch and accumulate in position order.
 template <int U, class M, typename Acc, class X>
-__device__ __forceinline__ void run_segment(const M& mat, const X& xr, const Segment& S,
-                                            Acc* __restrict__ state, double* __restrict__ y,
-                                            uint32_t lane) {
+__device__ __forceinline__ void consume_batch(const typename M::Raw* r, uint32_t mask, const X& xr,
+                                              Acc& acc) {
+  using Ops = AccOps<Acc>;
+  Acc xv[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) xv[u] = xr(M::c_of(r[u]));
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const Acc t = Ops::add(acc, Ops::prod(M::v_of(r[u]), xv[u]));
+    acc = (mask & (1u << u)) ? t : acc;
+  }
+}
+
+// Drain one tile's segment pool on one warp, software-pipelined across segment boundaries: the
+// next batch -- of the current segment, or batch 0 of the next segment -- is in flight while the
+// current batch is consumed; the next segment's descriptor is claimed one segment ahead.
+template <int U, class M, typename Acc, class GrabFn>
+__device__ __forceinline__ void run_segments(const M& mat, const XWindow<Acc>& xw,
+                                             const XGlobal<Acc>& xg, GrabFn&& grab,
+                                             Acc* __restrict__ state, double* __restrict__ y,
+                                             uint32_t lane) {
   using Ops = AccOps<Acc>;
   using Raw = typename M::Raw;
-  const uint64_t p0 = S.p0, p1 = S.p0 + S.n;
-  uint64_t base = p0 - S.lane0;
-  // head chunk (positions before p0 belong to the row's previous segment) and the first full
-  // batch are issued together, before anything is consumed
-  const uint64_t jh = base + lane;
-  const bool head = jh >= p0 && jh < p1;
-  Raw rh{};
-  if (head) rh = mat.load(jh);
-  base += 32;
-  const uint64_t nb = base < p1 ? (p1 - base) / (32 * U) : 0;
+  Segment sd;
+  if (!grab(sd)) return;
+  SegRun cur = seg_run<U>(sd);
+  Segment sn;
+  bool have_next = grab(sn);
   Raw ra[U], rb[U];
-  Acc acc;
-  auto load = [&](Raw* r, uint64_t b) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) r[u] = mat.load(b + lane + 32 * u);
+  const uint32_t safe = xw.xlo;
+  uint32_t ma = load_batch<U>(mat, ra, cur, 0, lane, safe), mb = 0;
+  auto init = [&](const SegRun& s) {
+    return (s.flags & kSegFirst) ? Acc(0) : state[static_cast<uint64_t>(s.slot) * 32 + lane];
   };
-  auto consume = [&](const Raw* r) {
-    Acc xv[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) xv[u] = xr(M::c_of(r[u]));
-#pragma unroll
-    for (int u = 0; u < U; ++u) acc = Ops::add(acc, Ops::prod(M::v_of(r[u]), xv[u]));
-  };
-  if (nb) load(ra, base);
-  acc = (S.flags & kSegFirst) ? Acc(0) : state[static_cast<uint64_t>(S.slot) * 32 + lane];
-  if (head) acc = Ops::add(acc, Ops::prod(M::v_of(rh), xr(M::c_of(rh))));
-  for (uint64_t k = 0; k < nb; k += 2) {  // ping-pong: the next batch is in flight during consume
-    if (k + 1 < nb) load(rb, base + 32 * U);
-    consume(ra);
-    base += 32 * U;
-    if (k + 1 >= nb) break;
-    if (k + 2 < nb) load(ra, base + 32 * U);
-    consume(rb);
-    base += 32 * U;
-  }
-  for (; base < p1; base += 32) {
-    const uint64_t j = base + lane;
-    if (j < p1) {
-      const Raw e = mat.load(j);
-      acc = Ops::add(acc, Ops::prod(M::v_of(e), xr(M::c_of(e))));
+  Acc acc = init(cur);
+  uint32_t bi = 0;
+  // one pipeline step: consume (rc, mc), prefetch into (rn, mn); false when the pool is drained
+  auto step = [&](const Raw* rc, uint32_t mc, Raw* rn, uint32_t& mn) -> bool {
+    const bool more = bi + 1 < cur.nbatch;
+    if (more) mn = load_batch<U>(mat, rn, cur, bi + 1, lane, safe);
+    else if (have_next) mn = load_batch<U>(mat, rn, seg_run<U>(sn), 0, lane, safe);
+    if (cur.flags & kSegGlobalX) consume_batch<U, M>(rc, mc, xg, acc);
+    else consume_batch<U, M>(rc, mc, xw, acc);
+    if (more) {
+      ++bi;
+      return true;
     }
-  }
-  if (S.flags & kSegLast) {
+    if (cur.flags & kSegLast) {
 #pragma unroll
-    for (int off = 16; off >= 1; off /= 2) acc = Ops::add(acc, __shfl_down_sync(kFull, acc, off));
-    if (lane == 0) y[S.row] = static_cast<double>(acc);
-  } else {
-    state[static_cast<uint64_t>(S.slot) * 32 + lane] = acc;
+      for (int off = 16; off >= 1; off /= 2) acc = Ops::add(acc, __shfl_down_sync(kFull, acc, off));
+      if (lane == 0) y[cur.row] = static_cast<double>(acc);
+    } else {
+      state[static_cast<uint64_t>(cur.slot) * 32 + lane] = acc;
+    }
+    if (!have_next) return false;
+    cur = seg_run<U>(sn);
+    bi = 0;
+    acc = init(cur);
+    have_next = grab(sn);
+    return true;
+  };
+  for (;;) {
+    if (!step(ra, ma, rb, mb)) break;
+    if (!step(rb, mb, ra, ma)) break;
   }
 }
 
@@ -199,26 +249,15 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     const XWindow<Acc> xw{xbuf0 + b * wcap, T.xlo};
     const XGlobal<Acc> xg{x};
     const uint32_t nseg = T.seg1 - T.seg0;
-    auto grab = [&]() {
+    auto grab = [&](Segment& s) -> bool {
       uint32_t k = 0;
       if (lane == 0) k = atomicAdd(&seg_next[b], 1u);
-      return __shfl_sync(kFull, k, 0);
+      k = __shfl_sync(kFull, k, 0);
+      if (k >= nseg) return false;
+      s = segs[T.seg0 + k];
+      return true;
     };
-    // the next segment's descriptor is claimed and loaded while the current one streams
-    uint32_t k = grab();
-    Segment S{};
-    if (k < nseg) S = segs[T.seg0 + k];
-    while (k < nseg) {
-      const uint32_t k2 = grab();
-      Segment S2{};
-      if (k2 < nseg) S2 = segs[T.seg0 + k2];
-      if (S.flags & kSegGlobalX)
-        run_segment<U>(mat, xg, S, state, y, lane);
-      else
-        run_segment<U>(mat, xw, S, state, y, lane);
-      k = k2;
-      S = S2;
-    }
+    run_segments<U>(mat, xw, xg, grab, state, y, lane);
     __syncwarp();
     if (lane == 0) {
       __threadfence_block();  // this warp's reads of buffer b happen before the count
