@@ -294,14 +294,37 @@ def run_ours(args):
     assert np.array_equal(yh.numpy().view(np.uint64), y.cpu().numpy().view(np.uint64)), \
         "host-path d differs from device-path d"
 
+    # N > 1: the dose slices all-gathered over NCCL into the full d on every rank (8(e)),
+    # timed separately from the sharded-resident step
+    gather_ms = 0.0
+    if dist:
+        from paper_2103_09683_b200.sharded import gather_dose
+        bnd = np.array([0] * (world + 1), dtype=np.uint64)
+        if world > 1:
+            bnd = bounds
+        for _ in range(2):
+            step()
+            gather_dose(y, bnd)
+        torch.cuda.synchronize()
+        dist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        for _ in range(e2e_steps):
+            step()
+            full = gather_dose(y, bnd)
+        g1.record()
+        torch.cuda.synchronize()
+        gather_ms = g0.elapsed_time(g1)
+        assert full.numel() == rows
+
     model_bytes = info["model_bytes"]
-    vals = torch.tensor([ms, e2e_ms], dtype=torch.float64, device="cuda")
+    vals = torch.tensor([ms, e2e_ms, gather_ms], dtype=torch.float64, device="cuda")
     sums = torch.tensor([float(model_bytes), float(info["nnz"]), 8.0 * cols, 8.0 * info["rows"]],
                         dtype=torch.float64, device="cuda")
     if dist:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
         dist.all_reduce(sums, op=dist.ReduceOp.SUM)
-    ms, e2e_ms = vals.tolist()
+    ms, e2e_ms, gather_ms = vals.tolist()
     total_bytes, total_nnz, h2d, d2h = sums.tolist()
     ms_step = ms / args.steps
     e2e_step = e2e_ms / e2e_steps
@@ -353,6 +376,7 @@ def run_ours(args):
                 "ms_per_step": e2e_step, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(info["n_kernels"]) * args.steps * world,
+        "ms_per_step_gathered": (gather_ms / e2e_steps) if world > 1 else None,
         "clocks": clk,
     }
     if world == 1 and not args.no_cpu_baseline:

@@ -208,7 +208,7 @@ int launch_tiles(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t 
   if constexpr (std::is_same_v<M, Packed16>) {
     switch (h->tile_cfg) {
       case 1: return launch_tiles_cfg<M, Acc, 32, 4>(h, mat, x, y, s);
-      case 2: return launch_tiles_cfg<M, Acc, 32, 8>(h, mat, x, y, s);
+      case 2: return launch_tiles_cfg<M, Acc, 24, 8>(h, mat, x, y, s);
       case 3: return launch_tiles_cfg<M, Acc, 16, 16>(h, mat, x, y, s);
       case 4: return launch_tiles_cfg<M, Acc, 32, 6>(h, mat, x, y, s);
       default: break;

@@ -41,7 +41,7 @@ struct Handle {
   uint64_t plan_bytes = 0, nonempty_rows = 0;
   // ... and column-windowed tiles of row segments, per wave (plan.cu, spmv_tiles.cuh)
   static constexpr uint32_t kMaxWaves = 32;
-  static constexpr int kTileWarps = 24;
+  static constexpr int kTileWarps = 32;
   static constexpr int kTileUnroll = 8;
   uint32_t acc_bytes = 8;          // shared-memory x element: 8 exact, 4 fp32
   uint32_t window_cols = 0;        // x window capacity per buffer (columns)

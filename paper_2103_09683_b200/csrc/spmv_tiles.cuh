@@ -111,15 +111,25 @@ __device__ __forceinline__ SegRun seg_run(const Segment& S) {
 // Issue batch b of segment s: U predicated requests (one 128-B request per chunk for Packed16).
 // Masked-off lanes get a filler element whose column (`safe_col`, the tile's window start) is a
 // valid x index, so the gather below needs no predicate; only the accumulation is masked.
+// Interior batches (every lane's U chunks inside the segment; warp-uniform test) load unmasked
+// and report kFullMask; edge batches are masked per chunk.
+template <int U>
+constexpr uint32_t kFullMask = (1u << U) - 1u;
+
 template <int U, class M>
 __device__ __forceinline__ uint32_t load_batch(const M& mat, typename M::Raw* r, const SegRun& s,
                                                uint32_t b, uint32_t lane, uint32_t safe_col) {
+  const uint32_t b0 = b * (32 * U);
+  const uint64_t base = s.base0 + b0 + lane;
+  if (b0 >= s.lo && b0 + 32 * U <= s.hi) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) r[u] = mat.load(base + 32 * u);
+    return kFullMask<U>;
+  }
   uint32_t mask = 0;
-  const uint32_t rel0 = b * (32 * U) + lane;
-  const uint64_t base = s.base0 + rel0;
 #pragma unroll
   for (int u = 0; u < U; ++u) {
-    const uint32_t rel = rel0 + 32 * u;
+    const uint32_t rel = b0 + lane + 32 * u;
     const bool ok = rel >= s.lo && rel < s.hi;
     r[u] = ok ? mat.load(base + 32 * u) : M::filler(safe_col);
     mask |= static_cast<uint32_t>(ok) << u;
@@ -127,7 +137,9 @@ __device__ __forceinline__ uint32_t load_batch(const M& mat, typename M::Raw* r,
   return mask;
 }
 
-// Gather x for a loaded batch and accumulate in position order.
+// Gather x for a loaded batch and accumulate in position order.  Masked chunks add +0.0, which
+// is the identity here: an accumulator that starts at +0.0 and only ever adds is never -0.0
+// (round-to-nearest turns exact cancellation into +0.0), and x + (+0.0) == x for x != -0.0.
 template <int U, class M, typename Acc, class X>
 __device__ __forceinline__ void consume_batch(const typename M::Raw* r, uint32_t mask, const X& xr,
                                               Acc& acc) {
@@ -135,10 +147,15 @@ __device__ __forceinline__ void consume_batch(const typename M::Raw* r, uint32_t
   Acc xv[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) xv[u] = xr(M::c_of(r[u]));
+  if (mask == kFullMask<U>) {
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const Acc t = Ops::add(acc, Ops::prod(M::v_of(r[u]), xv[u]));
-    acc = (mask & (1u << u)) ? t : acc;
+    for (int u = 0; u < U; ++u) acc = Ops::add(acc, Ops::prod(M::v_of(r[u]), xv[u]));
+  } else {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const Acc p = Ops::prod(M::v_of(r[u]), xv[u]);
+      acc = Ops::add(acc, (mask & (1u << u)) ? p : Acc(0));
+    }
   }
 }
 
