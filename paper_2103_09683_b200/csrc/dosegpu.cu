@@ -174,11 +174,11 @@ void launch_group(Handle* h, int b, const char* name, cudaStream_t s, const M& m
 
 // One persistent launch per wave (one CTA per SM): wave k continues the segments whose lane
 // partials wave k-1 stored.
-template <class M, typename Acc, int kWarps, int kU>
+template <class M, typename Acc, int kWarps, int kU, int kR = 0>
 int launch_tiles_cfg(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t s) {
-  const size_t smem = 2ull * h->window_cols * sizeof(Acc);
+  const size_t smem = 2ull * h->window_cols * sizeof(Acc) + ring_smem_bytes<kWarps, kR>();
   if (!h->tiles_attr) {  // a handle has one (M, Acc, config) and one device
-    DG_CUDA(cudaFuncSetAttribute(k_tiles<M, Acc, kWarps, kU>,
+    DG_CUDA(cudaFuncSetAttribute(k_tiles<M, Acc, kWarps, kU, kR>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
     h->tiles_attr = true;
@@ -189,7 +189,7 @@ int launch_tiles_cfg(Handle* h, const M& mat, const Acc* x, double* y, cudaStrea
   for (uint32_t w = 0; w < h->n_waves; ++w) {
     if (!h->wave_tiles[w]) continue;
     const int grid = std::min<int>(h->sm_count, static_cast<int>(h->wave_tiles[w]));
-    k_tiles<M, Acc, kWarps, kU><<<grid, kWarps * 32, smem, s>>>(
+    k_tiles<M, Acc, kWarps, kU, kR><<<grid, kWarps * 32, smem, s>>>(
         mat, x, static_cast<const Tile*>(h->d_tiles[w]), h->wave_tiles[w],
         static_cast<const Segment*>(h->d_segs[w]), static_cast<Acc*>(h->d_state), y,
         h->d_counters + w, h->window_cols);
@@ -211,10 +211,27 @@ int launch_tiles(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t 
       case 2: return launch_tiles_cfg<M, Acc, 24, 8>(h, mat, x, y, s);
       case 3: return launch_tiles_cfg<M, Acc, 16, 16>(h, mat, x, y, s);
       case 4: return launch_tiles_cfg<M, Acc, 32, 6>(h, mat, x, y, s);
+      case 5: return launch_tiles_cfg<M, Acc, 32, 8, 3>(h, mat, x, y, s);
+      case 6: return launch_tiles_cfg<M, Acc, 24, 8, 4>(h, mat, x, y, s);
+      case 7: return launch_tiles_cfg<M, Acc, 32, 8, 4>(h, mat, x, y, s);
       default: break;
     }
   }
   return launch_tiles_cfg<M, Acc, Handle::kTileWarps, Handle::kTileUnroll>(h, mat, x, y, s);
+}
+
+// Bytes of one x-window buffer for a tile configuration: what is left of the 227 KB of shared
+// memory per CTA after the TMA rings, split in two buffers, rounded down to 1 KB.
+uint32_t window_bytes_for(int cfg, bool packed) {
+  constexpr size_t kMaxDyn = 232448 - 256;  // cudaDevAttrMaxSharedMemoryPerBlockOptin - static
+  size_t ring = 0;
+  if (packed) {
+    if (cfg == 5) ring = ring_smem_bytes<32, 3>();
+    if (cfg == 6) ring = ring_smem_bytes<24, 4>();
+    if (cfg == 7) ring = ring_smem_bytes<32, 4>();
+  }
+  if (!ring) return kWindowBytes;
+  return static_cast<uint32_t>(((kMaxDyn - ring) / 2) & ~size_t(1023));
 }
 
 template <class M>
@@ -295,9 +312,9 @@ int finish_create(Handle* h, const std::vector<uint64_t>& lens) {
   const char* plan = std::getenv("DG_PLAN");  // "warp": v0 warp-per-row plan (A/B only)
   h->use_tiles = h->lane_width == 32 && !(plan && std::strcmp(plan, "warp") == 0);
   h->acc_bytes = h->accumulation == DG_ACCUM_FP32 ? 4 : 8;
-  h->window_cols = kWindowBytes / h->acc_bytes;
   if (const char* tn = std::getenv("DG_TILE_NNZ")) h->tile_nnz = std::strtoull(tn, nullptr, 10);
   if (const char* tc = std::getenv("DG_TILE_CFG")) h->tile_cfg = std::atoi(tc);
+  h->window_cols = window_bytes_for(h->tile_cfg, h->packed) / h->acc_bytes;
   DG_TRY(build_plan(h, lens));
   if (h->use_tiles) DG_TRY(plan_tiles(h, lens));
   // x staging is padded to a 16-byte multiple: the 1-D TMA moves 16-byte granules
@@ -426,7 +443,8 @@ int dg_create(const dg_csr_view* v, const dg_options* opts_in, dg_handle** out) 
   // --- (binary16, u16): one packed 32-bit stream, same 4 bytes per nonzero --------------------
   const char* nopack = std::getenv("DG_NO_PACK");
   if (h->value_precision == DG_HALF && h->index_bytes == 2 && !(nopack && *nopack == '1')) {
-    if ((st = cu(cudaMalloc(&h->d_packed, nz * 4)))) return fail(st);
+    // +16 B: the 1-D TMA of the stream rounds a batch up to whole 16-byte granules
+    if ((st = cu(cudaMalloc(&h->d_packed, nz * 4 + 16)))) return fail(st);
     dg::k_pack16<<<dg::grid_for(shard_nnz, 256), 256>>>(static_cast<const uint16_t*>(h->d_col),
                                                         static_cast<const uint16_t*>(h->d_val),
                                                         h->d_packed, shard_nnz);

@@ -251,7 +251,7 @@ int dg_create_generated(const dg_profile* p, uint32_t n_beams, uint32_t index_by
   const uint64_t nz = std::max<uint64_t>(h->nnz, 1);
   const char* nopack = std::getenv("DG_NO_PACK");
   if (index_bytes == 2 && !(nopack && *nopack == '1')) {  // (binary16, u16): Packed16 stream
-    if ((st = cu(cudaMalloc(&h->d_packed, nz * 4)))) return fail(st);
+    if ((st = cu(cudaMalloc(&h->d_packed, nz * 4 + 16)))) return fail(st);  // TMA granule pad
     h->packed = true;
     dg::k_gen_fill<uint16_t><<<dg::grid_for(n, 128), 128>>>(beams, r0, n, h->d_row_ptr, nullptr,
                                                            nullptr, h->d_packed);

@@ -213,8 +213,124 @@ __device__ __forceinline__ void run_segments(const M& mat, const XWindow<Acc>& x
   }
 }
 
-// Persistent: one CTA per SM; dynamic smem = 2 * wcap * sizeof(Acc) (two x-window buffers).
-template <class M, typename Acc, int WARPS, int U>
+// ---- TMA ring variant (Packed16): each warp streams its segments' batches into a private ring
+// of R shared-memory stages with 1-D bulk copies issued by lane 0, so R-1 batches (~1 KB each)
+// are in flight per warp without holding registers.  Stage t carries a copy of its batch's
+// descriptor; batches are consumed in issue order, which is segment order, which is lane-partial
+// order -- so the accumulation order is exactly the register pipeline's.
+constexpr uint32_t kStageElems = 264;  // 256 positions + up to 3 + 3 alignment slack, x 4 B
+
+struct StageMeta {
+  uint64_t base0;
+  uint32_t lo, hi, k, nbatch, row, slot, flags, al;  // al: element offset of stage[0] from base0
+};
+
+template <int U, int R, typename Acc, class GrabFn>
+__device__ __forceinline__ void run_segments_tma(const Packed16& mat, const XWindow<Acc>& xw,
+                                                 const XGlobal<Acc>& xg, GrabFn&& grab,
+                                                 Acc* __restrict__ state, double* __restrict__ y,
+                                                 uint32_t lane, uint32_t* ring, StageMeta* meta,
+                                                 uint64_t* bars, uint32_t& parity) {
+  static_assert(U * 32 == 256, "stage layout assumes 256-position batches");
+  using Ops = AccOps<Acc>;
+  // producer cursor: meaningful in lane 0 only
+  SegRun pseg{};
+  uint32_t pk = 0;
+  Segment pre{};
+  bool have_pre = false, have_cur = false;
+  {
+    Segment s0;
+    if (grab(s0)) {
+      pseg = seg_run<U>(s0);
+      have_cur = true;
+      have_pre = grab(pre);
+    }
+  }
+  // issue the next batch into stage t; returns whether anything was issued (warp-uniform)
+  auto issue = [&](int t) -> bool {
+    if (have_cur && pk == pseg.nbatch) {
+      have_cur = have_pre;
+      if (have_cur) {
+        pseg = seg_run<U>(pre);
+        pk = 0;
+        have_pre = grab(pre);
+      }
+    }
+    if (!have_cur) return false;
+    if (lane == 0) {
+      const uint32_t b0 = pk * 256u;
+      const uint32_t rs = max(pseg.lo, b0), re = min(pseg.hi, b0 + 256u);
+      const uint64_t start = pseg.base0 + rs, end = pseg.base0 + re;
+      const uint64_t lo_al = start & ~3ull, hi_al = (end + 3) & ~3ull;
+      StageMeta m;
+      m.base0 = pseg.base0;
+      m.lo = pseg.lo;
+      m.hi = pseg.hi;
+      m.k = pk;
+      m.nbatch = pseg.nbatch;
+      m.row = pseg.row;
+      m.slot = pseg.slot;
+      m.flags = pseg.flags;
+      m.al = static_cast<uint32_t>(lo_al - pseg.base0);
+      meta[t] = m;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // WAR on ring[t]
+      const uint32_t bytes = static_cast<uint32_t>(hi_al - lo_al) * 4u;
+      mbar_arrive_expect_tx(&bars[t], bytes);
+      tma_load_1d(ring + t * kStageElems, mat.w + lo_al, bytes, &bars[t]);
+    }
+    ++pk;
+    return true;
+  };
+  int inflight = 0;
+#pragma unroll
+  for (int t = 0; t < R; ++t)
+    if (issue(t)) ++inflight;
+  Acc acc = Acc(0);
+  int cs = 0;
+  while (inflight > 0) {
+    mbar_wait(&bars[cs], (parity >> cs) & 1u);
+    parity ^= 1u << cs;
+    const StageMeta m = meta[cs];
+    if (m.k == 0)
+      acc = (m.flags & kSegFirst) ? Acc(0) : state[static_cast<uint64_t>(m.slot) * 32 + lane];
+    const uint32_t* st = ring + cs * kStageElems;
+    uint32_t raw[U];
+    uint32_t mask = 0;
+    const uint32_t b0 = m.k * 256u + lane;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t rel = b0 + 32 * u;
+      const bool ok = rel >= m.lo && rel < m.hi;
+      raw[u] = ok ? st[rel - m.al] : Packed16::filler(xw.xlo);
+      mask |= static_cast<uint32_t>(ok) << u;
+    }
+    if (m.flags & kSegGlobalX) consume_batch<U, Packed16>(raw, mask, xg, acc);
+    else consume_batch<U, Packed16>(raw, mask, xw, acc);
+    if (m.k + 1 == m.nbatch) {
+      if (m.flags & kSegLast) {
+#pragma unroll
+        for (int off = 16; off >= 1; off /= 2) acc = Ops::add(acc, __shfl_down_sync(kFull, acc, off));
+        if (lane == 0) y[m.row] = static_cast<double>(acc);
+      } else {
+        state[static_cast<uint64_t>(m.slot) * 32 + lane] = acc;
+      }
+    }
+    --inflight;
+    __syncwarp();  // every lane is done reading stage cs before it is refilled
+    if (issue(cs)) ++inflight;
+    cs = cs + 1 == R ? 0 : cs + 1;
+  }
+}
+
+// Shared memory of k_tiles beyond the two x-window buffers.
+template <int WARPS, int R>
+constexpr size_t ring_smem_bytes() {
+  return R > 0 ? static_cast<size_t>(WARPS) * R * (kStageElems * 4 + sizeof(StageMeta) + 8) : 0;
+}
+
+// Persistent: one CTA per SM; dynamic smem = 2 * wcap * sizeof(Acc) (two x-window buffers)
+// + ring_smem_bytes<WARPS, R>() (R > 0: TMA-streamed matrix, Packed16 only).
+template <class M, typename Acc, int WARPS, int U, int R = 0>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     k_tiles(M mat, const Acc* __restrict__ x, const Tile* __restrict__ tiles, uint32_t n_tiles,
             const Segment* __restrict__ segs, Acc* __restrict__ state, double* __restrict__ y,
@@ -246,10 +362,30 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     }
   };
 
+  // TMA ring carve-up (R > 0): per warp R stages, R stage descriptors, R mbarriers
+  const uint32_t warp = threadIdx.x >> 5;
+  uint32_t* my_ring = nullptr;
+  StageMeta* my_meta = nullptr;
+  uint64_t* my_bars = nullptr;
+  uint32_t ring_parity = 0;
+  if constexpr (R > 0) {
+    unsigned char* p = smem_raw + 2ull * wcap * sizeof(Acc);
+    uint32_t* rings = reinterpret_cast<uint32_t*>(p);
+    StageMeta* metas = reinterpret_cast<StageMeta*>(p + WARPS * R * kStageElems * 4);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(p + WARPS * R * kStageElems * 4 +
+                                                 WARPS * R * sizeof(StageMeta));
+    my_ring = rings + warp * R * kStageElems;
+    my_meta = metas + warp * R;
+    my_bars = bars + warp * R;
+    if (lane < R) mbar_init(&my_bars[lane], 1);
+  }
   if (threadIdx.x == 0) {
     mbar_init(&full[0], 1);
     mbar_init(&full[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0) {
     refill(0);
     refill(1);
   }
@@ -274,7 +410,12 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       s = segs[T.seg0 + k];
       return true;
     };
-    run_segments<U>(mat, xw, xg, grab, state, y, lane);
+    if constexpr (R > 0) {
+      run_segments_tma<U, R>(mat, xw, xg, grab, state, y, lane, my_ring, my_meta, my_bars,
+                             ring_parity);
+    } else {
+      run_segments<U>(mat, xw, xg, grab, state, y, lane);
+    }
     __syncwarp();
     if (lane == 0) {
       __threadfence_block();  // this warp's reads of buffer b happen before the count
