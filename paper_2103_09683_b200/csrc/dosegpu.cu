@@ -174,11 +174,11 @@ void launch_group(Handle* h, int b, const char* name, cudaStream_t s, const M& m
 
 // One persistent launch per wave (one CTA per SM): wave k continues the segments whose lane
 // partials wave k-1 stored.
-template <class M, typename Acc, int kWarps, int kU, int kR = 0>
+template <class M, typename Acc, int kWarps, int kU, int kR = 0, int kP = 0>
 int launch_tiles_cfg(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t s) {
   const size_t smem = 2ull * h->window_cols * sizeof(Acc) + ring_smem_bytes<kWarps, kR>();
   if (!h->tiles_attr) {  // a handle has one (M, Acc, config) and one device
-    DG_CUDA(cudaFuncSetAttribute(k_tiles<M, Acc, kWarps, kU, kR>,
+    DG_CUDA(cudaFuncSetAttribute(k_tiles<M, Acc, kWarps, kU, kR, kP>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
     h->tiles_attr = true;
@@ -189,7 +189,7 @@ int launch_tiles_cfg(Handle* h, const M& mat, const Acc* x, double* y, cudaStrea
   for (uint32_t w = 0; w < h->n_waves; ++w) {
     if (!h->wave_tiles[w]) continue;
     const int grid = std::min<int>(h->sm_count, static_cast<int>(h->wave_tiles[w]));
-    k_tiles<M, Acc, kWarps, kU, kR><<<grid, kWarps * 32, smem, s>>>(
+    k_tiles<M, Acc, kWarps, kU, kR, kP><<<grid, kWarps * 32, smem, s>>>(
         mat, x, static_cast<const Tile*>(h->d_tiles[w]), h->wave_tiles[w],
         static_cast<const Segment*>(h->d_segs[w]), static_cast<Acc*>(h->d_state), y,
         h->d_counters + w, h->window_cols);
@@ -211,9 +211,10 @@ int launch_tiles(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t 
       case 2: return launch_tiles_cfg<M, Acc, 24, 8>(h, mat, x, y, s);
       case 3: return launch_tiles_cfg<M, Acc, 16, 16>(h, mat, x, y, s);
       case 4: return launch_tiles_cfg<M, Acc, 32, 6>(h, mat, x, y, s);
-      case 5: return launch_tiles_cfg<M, Acc, 32, 8, 3>(h, mat, x, y, s);
       case 6: return launch_tiles_cfg<M, Acc, 24, 8, 4>(h, mat, x, y, s);
-      case 7: return launch_tiles_cfg<M, Acc, 32, 8, 4>(h, mat, x, y, s);
+      case 8: return launch_tiles_cfg<M, Acc, 32, 8, 0, 1>(h, mat, x, y, s);
+      case 9: return launch_tiles_cfg<M, Acc, 32, 8, 0, 2>(h, mat, x, y, s);
+      case 10: return launch_tiles_cfg<M, Acc, 32, 8, 0, 4>(h, mat, x, y, s);
       default: break;
     }
   }
@@ -226,9 +227,7 @@ uint32_t window_bytes_for(int cfg, bool packed) {
   constexpr size_t kMaxDyn = 232448 - 256;  // cudaDevAttrMaxSharedMemoryPerBlockOptin - static
   size_t ring = 0;
   if (packed) {
-    if (cfg == 5) ring = ring_smem_bytes<32, 3>();
     if (cfg == 6) ring = ring_smem_bytes<24, 4>();
-    if (cfg == 7) ring = ring_smem_bytes<32, 4>();
   }
   if (!ring) return kWindowBytes;
   return static_cast<uint32_t>(((kMaxDyn - ring) / 2) & ~size_t(1023));

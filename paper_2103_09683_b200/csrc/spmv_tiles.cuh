@@ -21,6 +21,8 @@
 // boundaries, where the lane partials are stored and reloaded unchanged.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "spmv_kernels.cuh"
 
@@ -137,6 +139,21 @@ __device__ __forceinline__ uint32_t load_batch(const M& mat, typename M::Raw* r,
   return mask;
 }
 
+// L2 prefetch of batches [b, b + P) of segment s: lane l touches chunk l % 8 of batch b + l / 8.
+// Prefetches hold no registers, so the stream runs P batches ahead of the register pipeline.
+template <int U, int P, class M>
+__device__ __forceinline__ void prefetch_batches(const M& mat, const SegRun& s, uint32_t b,
+                                                 uint32_t lane) {
+  if constexpr (P > 0 && std::is_same_v<M, Packed16>) {
+    static_assert(U == 8, "one lane per 128-byte chunk of an 8-chunk batch");
+    if (lane < 8 * P) {
+      const uint32_t rel = (b + lane / 8) * (32 * U) + (lane % 8) * 32;
+      if (rel < s.hi)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(mat.w + s.base0 + rel));
+    }
+  }
+}
+
 // Gather x for a loaded batch and accumulate in position order.  Masked chunks add +0.0, which
 // is the identity here: an accumulator that starts at +0.0 and only ever adds is never -0.0
 // (round-to-nearest turns exact cancellation into +0.0), and x + (+0.0) == x for x != -0.0.
@@ -162,7 +179,7 @@ __device__ __forceinline__ void consume_batch(const typename M::Raw* r, uint32_t
 // Drain one tile's segment pool on one warp, software-pipelined across segment boundaries: the
 // next batch -- of the current segment, or batch 0 of the next segment -- is in flight while the
 // current batch is consumed; the next segment's descriptor is claimed one segment ahead.
-template <int U, class M, typename Acc, class GrabFn>
+template <int U, int P, class M, typename Acc, class GrabFn>
 __device__ __forceinline__ void run_segments(const M& mat, const XWindow<Acc>& xw,
                                              const XGlobal<Acc>& xg, GrabFn&& grab,
                                              Acc* __restrict__ state, double* __restrict__ y,
@@ -177,6 +194,7 @@ __device__ __forceinline__ void run_segments(const M& mat, const XWindow<Acc>& x
   Raw ra[U], rb[U];
   const uint32_t safe = xw.xlo;
   uint32_t ma = load_batch<U>(mat, ra, cur, 0, lane, safe), mb = 0;
+  prefetch_batches<U, P>(mat, cur, 1, lane);
   auto init = [&](const SegRun& s) {
     return (s.flags & kSegFirst) ? Acc(0) : state[static_cast<uint64_t>(s.slot) * 32 + lane];
   };
@@ -187,6 +205,11 @@ __device__ __forceinline__ void run_segments(const M& mat, const XWindow<Acc>& x
     const bool more = bi + 1 < cur.nbatch;
     if (more) mn = load_batch<U>(mat, rn, cur, bi + 1, lane, safe);
     else if (have_next) mn = load_batch<U>(mat, rn, seg_run<U>(sn), 0, lane, safe);
+    if constexpr (P > 0) {  // the L2 prefetch stream runs P batches ahead of the loads
+      const uint32_t pf = bi + 1 + P;
+      if (pf < cur.nbatch) prefetch_batches<U, 1>(mat, cur, pf, lane);
+      else if (have_next) prefetch_batches<U, 1>(mat, seg_run<U>(sn), pf - cur.nbatch, lane);
+    }
     if (cur.flags & kSegGlobalX) consume_batch<U, M>(rc, mc, xg, acc);
     else consume_batch<U, M>(rc, mc, xw, acc);
     if (more) {
@@ -330,7 +353,7 @@ constexpr size_t ring_smem_bytes() {
 
 // Persistent: one CTA per SM; dynamic smem = 2 * wcap * sizeof(Acc) (two x-window buffers)
 // + ring_smem_bytes<WARPS, R>() (R > 0: TMA-streamed matrix, Packed16 only).
-template <class M, typename Acc, int WARPS, int U, int R = 0>
+template <class M, typename Acc, int WARPS, int U, int R = 0, int P = 0>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     k_tiles(M mat, const Acc* __restrict__ x, const Tile* __restrict__ tiles, uint32_t n_tiles,
             const Segment* __restrict__ segs, Acc* __restrict__ state, double* __restrict__ y,
@@ -414,7 +437,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       run_segments_tma<U, R>(mat, xw, xg, grab, state, y, lane, my_ring, my_meta, my_bars,
                              ring_parity);
     } else {
-      run_segments<U>(mat, xw, xg, grab, state, y, lane);
+      run_segments<U, P>(mat, xw, xg, grab, state, y, lane);
     }
     __syncwarp();
     if (lane == 0) {
