@@ -215,8 +215,14 @@ int launch_tiles(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t 
       case 8: return launch_tiles_cfg<M, Acc, 32, 8, 0, 1>(h, mat, x, y, s);
       case 9: return launch_tiles_cfg<M, Acc, 32, 8, 0, 2>(h, mat, x, y, s);
       case 10: return launch_tiles_cfg<M, Acc, 32, 8, 0, 4>(h, mat, x, y, s);
+      case 11: return launch_tiles_cfg<M, Acc, 32, 8, 0, 0>(h, mat, x, y, s);
       default: break;
     }
+    // measured on C2 (profiles/): L2 prefetch 2 batches ahead (exact) / 4 ahead (fp32)
+    if constexpr (std::is_same_v<Acc, float>)
+      return launch_tiles_cfg<M, Acc, Handle::kTileWarps, Handle::kTileUnroll, 0, 4>(h, mat, x, y, s);
+    else
+      return launch_tiles_cfg<M, Acc, Handle::kTileWarps, Handle::kTileUnroll, 0, 2>(h, mat, x, y, s);
   }
   return launch_tiles_cfg<M, Acc, Handle::kTileWarps, Handle::kTileUnroll>(h, mat, x, y, s);
 }
