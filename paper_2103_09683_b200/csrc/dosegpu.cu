@@ -184,6 +184,13 @@ int launch_tiles_cfg(Handle* h, const M& mat, const Acc* x, double* y, cudaStrea
     h->tiles_attr = true;
   }
   DG_CUDA(cudaMemsetAsync(h->d_counters, 0, Handle::kMaxWaves * sizeof(uint32_t), s));
+  BlockSignal sig{nullptr, nullptr, 0};
+  if (h->signal_blocks) {
+    DG_CUDA(cudaMemcpyAsync(h->d_blk_left, h->d_blk_left_init, h->n_blocks * sizeof(uint32_t),
+                            cudaMemcpyDeviceToDevice, s));
+    sig = {h->d_blk_left, h->d_blk_flag, h->epoch};
+  }
+  DG_CUDA(cudaEventRecord(h->ev_tiles_start, s));  // every row not owned by a tile is final here
   static const char* const kWaveName[] = {"[w0]", "[w1]", "[w2]", "[w3]", "[w4]", "[w5]",
                                           "[w6]", "[w7]", "[w8+]"};
   for (uint32_t w = 0; w < h->n_waves; ++w) {
@@ -192,7 +199,7 @@ int launch_tiles_cfg(Handle* h, const M& mat, const Acc* x, double* y, cudaStrea
     k_tiles<M, Acc, kWarps, kU, kR, kP><<<grid, kWarps * 32, smem, s>>>(
         mat, x, static_cast<const Tile*>(h->d_tiles[w]), h->wave_tiles[w],
         static_cast<const Segment*>(h->d_segs[w]), static_cast<Acc*>(h->d_state), y,
-        h->d_counters + w, h->window_cols);
+        h->d_counters + w, h->window_cols, sig);
     h->post(s, kWaveName[std::min<uint32_t>(w, 8)], h->wave_rows[w], h->wave_nnz[w]);
   }
   DG_CUDA(cudaGetLastError());
@@ -332,7 +339,25 @@ int finish_create(Handle* h, const std::vector<uint64_t>& lens) {
   }
   for (auto& e : h->ev) DG_CUDA(cudaEventCreate(&e));
   for (auto& e : h->kev) DG_CUDA(cudaEventCreate(&e));
+  DG_CUDA(cudaEventCreateWithFlags(&h->ev_tiles_start, cudaEventDisableTiming));
+  DG_CUDA(cudaEventCreateWithFlags(&h->ev_d2h_done, cudaEventDisableTiming));
+  DG_CUDA(cudaStreamCreateWithFlags(&h->d2h_stream, cudaStreamNonBlocking));
   return DG_OK;
+}
+
+// cuStreamWaitValue32 through the runtime's driver entry-point query (no libcuda link needed).
+WaitValueFn wait_value_fn() {
+  static const WaitValueFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return static_cast<WaitValueFn>(nullptr);
+    }
+    return reinterpret_cast<WaitValueFn>(p);
+  }();
+  return fn;
 }
 
 }  // namespace dg
@@ -485,6 +510,15 @@ int dg_destroy(dg_handle* hh) {
   }
   cudaFree(h->d_state);
   cudaFree(h->d_counters);
+  cudaFree(h->d_blk_left);
+  cudaFree(h->d_blk_left_init);
+  cudaFree(h->d_blk_flag);
+  if (h->d2h_stream) {
+    cudaStreamSynchronize(h->d2h_stream);
+    cudaStreamDestroy(h->d2h_stream);
+  }
+  if (h->ev_tiles_start) cudaEventDestroy(h->ev_tiles_start);
+  if (h->ev_d2h_done) cudaEventDestroy(h->ev_d2h_done);
   for (auto e : h->ev)
     if (e) cudaEventDestroy(e);
   for (auto e : h->kev)
@@ -513,10 +547,34 @@ int dg_dose(dg_handle* hh, const double* x, uint64_t x_len, double* y, uint32_t 
                             x_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
   DG_CUDA(cudaEventRecord(h->ev[1], s));
   h->profiling = (flags & DG_PROFILE) != 0;
+  // Host d: download row block k as soon as the tile kernel publishes its completion, while it
+  // still works on later blocks (one wave only: with carried partials the last wave owns rows).
+  const char* no_ovl = std::getenv("DG_NO_OVERLAP");
+  const bool overlap = !y_dev && h->rows && h->use_tiles && h->n_waves == 1 &&
+                       h->n_blocks > 1 && dg::wait_value_fn() && !(no_ovl && *no_ovl == '1');
+  h->signal_blocks = overlap;
+  if (overlap) ++h->epoch;
   DG_TRY(dg::run_kernels(h, d_x, d_y, s));
   DG_CUDA(cudaEventRecord(h->ev[2], s));
-  if (!y_dev && h->rows)
+  if (overlap) {
+    DG_CUDA(cudaStreamWaitEvent(h->d2h_stream, h->ev_tiles_start, 0));
+    for (uint32_t k = 0; k < h->n_blocks; ++k) {
+      const uint64_t r0 = h->blk_row0[k], r1 = h->blk_row0[k + 1];
+      if (r1 == r0) continue;
+      if (h->blk_tiles[k]) {
+        const CUresult cr = dg::wait_value_fn()(
+            reinterpret_cast<CUstream>(h->d2h_stream),
+            reinterpret_cast<CUdeviceptr>(h->d_blk_flag + k), h->epoch, CU_STREAM_WAIT_VALUE_GEQ);
+        if (cr != CUDA_SUCCESS) return DG_ERR_CUDA_BASE + static_cast<int>(cudaErrorUnknown);
+      }
+      DG_CUDA(cudaMemcpyAsync(y + r0, h->d_y + r0, (r1 - r0) * sizeof(double),
+                              cudaMemcpyDeviceToHost, h->d2h_stream));
+    }
+    DG_CUDA(cudaEventRecord(h->ev_d2h_done, h->d2h_stream));
+    DG_CUDA(cudaStreamWaitEvent(s, h->ev_d2h_done, 0));
+  } else if (!y_dev && h->rows) {
     DG_CUDA(cudaMemcpyAsync(y, h->d_y, h->rows * sizeof(double), cudaMemcpyDeviceToHost, s));
+  }
   DG_CUDA(cudaEventRecord(h->ev[3], s));
   h->timing_valid = false;
   if (!(flags & DG_NO_SYNC) || !x_dev || !y_dev) {

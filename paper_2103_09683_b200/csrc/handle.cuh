@@ -1,6 +1,7 @@
 // handle.cuh -- the device-resident state behind a dg_handle.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -59,6 +60,19 @@ struct Handle {
   bool use_tiles = false;
   bool tiles_attr = false;
   int tile_cfg = 0;  // DG_TILE_CFG: alternative (warps, U) configurations for A/B
+
+  // output row blocks (plan.cu): the d download of block k overlaps the kernel's later blocks
+  static constexpr uint32_t kMaxBlocks = 8;
+  uint32_t n_blocks = 1;
+  uint64_t blk_row0[kMaxBlocks + 1] = {};
+  uint32_t blk_tiles[kMaxBlocks] = {};
+  uint32_t* d_blk_left = nullptr;       // per-dose countdown of unfinished tiles per block
+  uint32_t* d_blk_left_init = nullptr;  // the tile counts, copied into d_blk_left per dose
+  uint32_t* d_blk_flag = nullptr;       // epoch of the dose that last completed block k
+  uint32_t epoch = 0;
+  cudaStream_t d2h_stream = nullptr;
+  cudaEvent_t ev_tiles_start = nullptr, ev_d2h_done = nullptr;
+  bool signal_blocks = false;  // this dose publishes block completion (host d, overlapped D2H)
 
   // staging for host x / y and the fp32 family
   double* d_x = nullptr;
@@ -135,6 +149,9 @@ int dispatch_mat(const Handle* h, F&& f) {
                                            static_cast<const double*>(h->d_val)});
   }
 }
+
+typedef CUresult (*WaitValueFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WaitValueFn wait_value_fn();
 
 // shared by dosegpu.cu, plan.cu and generator.cu
 int select_device(int32_t want, int* dev_out);

@@ -165,59 +165,83 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
   if (waves.size() > Handle::kMaxWaves) return DG_ERR_UNSUPPORTED_FEATURE;
   h->n_waves = static_cast<uint32_t>(waves.size());
   h->n_global_rows = global_x.size();
+  // Output row blocks: contiguous, byte-balanced row ranges whose tiles are listed block after
+  // block, so block k of d is complete (and can be downloaded) while later blocks still run.
+  const uint32_t K = h->nnz >= (16ull << 20) ? Handle::kMaxBlocks : 1;
+  {
+    std::vector<uint64_t> b(K + 1);
+    std::vector<uint32_t> l32(rows);
+    for (uint64_t r = 0; r < rows; ++r) l32[r] = static_cast<uint32_t>(lens[r]);
+    dg_partition_lengths(l32.data(), rows, h->value_bytes + h->index_bytes, K, b.data());
+    h->n_blocks = K;
+    for (uint32_t k = 0; k <= K; ++k) h->blk_row0[k] = b[k];
+  }
+  auto blk_of = [&](uint32_t row) {
+    return static_cast<uint32_t>(std::upper_bound(h->blk_row0, h->blk_row0 + K + 1, row) -
+                                 h->blk_row0) - 1;
+  };
   for (uint32_t w = 0; w < h->n_waves; ++w) {
-    auto& S = waves[w];
-    std::stable_sort(S.begin(), S.end(), [](const HostSeg& a, const HostSeg& b) {
-      return a.clo != b.clo ? a.clo < b.clo : a.row < b.row;
-    });
+    std::vector<std::vector<HostSeg>> win(K), glob(K);
+    for (const HostSeg& s : waves[w]) win[blk_of(s.row)].push_back(s);
+    if (w == 0)
+      for (const HostSeg& s : global_x) glob[blk_of(s.row)].push_back(s);
     std::vector<Tile> tiles;
     std::vector<Segment> segs;
-    segs.reserve(S.size() + (w == 0 ? global_x.size() : 0));
+    segs.reserve(waves[w].size() + (w == 0 ? global_x.size() : 0));
     uint64_t wave_nnz = 0, wave_rows = 0;
-    if (w == 0 && !global_x.empty()) {
-      // global-x tiles first (no window), longest rows first: they are the longest work items
-      std::stable_sort(global_x.begin(), global_x.end(),
-                       [](const HostSeg& a, const HostSeg& b) { return a.n > b.n; });
+    for (uint32_t k = 0; k < K; ++k) {
+      // signalled only when one wave finishes every row (else the last wave owns the rows)
+      const uint16_t blk = h->n_waves == 1 ? static_cast<uint16_t>(k) : kNoBlock;
+      const size_t tiles_before = tiles.size();
+      // global-x tiles first (no window), longest rows first: the longest work items
+      auto& G = glob[k];
+      std::stable_sort(G.begin(), G.end(), [](const HostSeg& a, const HostSeg& b) { return a.n > b.n; });
       size_t g = 0;
-      while (g < global_x.size()) {
+      while (g < G.size()) {
         uint64_t nnz = 0;
         const uint32_t s0 = static_cast<uint32_t>(segs.size());
-        while (g < global_x.size() && (nnz == 0 || nnz + global_x[g].n <= h->tile_nnz)) {
-          const HostSeg& q = global_x[g++];
+        while (g < G.size() && (nnz == 0 || nnz + G[g].n <= h->tile_nnz)) {
+          const HostSeg& q = G[g++];
           segs.push_back({q.p0, q.n, q.row, 0, 0, q.flags});
           nnz += q.n;
           wave_nnz += q.n;
           ++wave_rows;
         }
-        tiles.push_back({0, 0, s0, static_cast<uint32_t>(segs.size())});
+        tiles.push_back({0, 0, blk, s0, static_cast<uint32_t>(segs.size())});
       }
-    }
-    size_t i = 0;
-    while (i < S.size()) {
-      const uint32_t xlo = S[i].clo / align * align;
-      uint32_t hi = S[i].chi;
-      uint64_t nnz = 0;
-      size_t j = i;
-      while (j < S.size()) {
-        const uint32_t nhi = std::max(hi, S[j].chi);
-        if (j > i && (static_cast<uint64_t>(nhi) - xlo + 1 > W || nnz + S[j].n > h->tile_nnz)) break;
-        hi = nhi;
-        nnz += S[j].n;
-        ++j;
+      // windowed tiles: segments by first column, cut at the window width or ~tile_nnz
+      auto& S = win[k];
+      std::stable_sort(S.begin(), S.end(), [](const HostSeg& a, const HostSeg& b) {
+        return a.clo != b.clo ? a.clo < b.clo : a.row < b.row;
+      });
+      size_t i = 0;
+      while (i < S.size()) {
+        const uint32_t xlo = S[i].clo / align * align;
+        uint32_t hi = S[i].chi;
+        uint64_t nnz = 0;
+        size_t j = i;
+        while (j < S.size()) {
+          const uint32_t nhi = std::max(hi, S[j].chi);
+          if (j > i && (static_cast<uint64_t>(nhi) - xlo + 1 > W || nnz + S[j].n > h->tile_nnz)) break;
+          hi = nhi;
+          nnz += S[j].n;
+          ++j;
+        }
+        // longest segment first inside the tile (warps pull segments dynamically)
+        std::stable_sort(S.begin() + i, S.begin() + j,
+                         [](const HostSeg& a, const HostSeg& b) { return a.n > b.n; });
+        uint32_t xlen = (hi - xlo + 1 + align - 1) / align * align;
+        if (xlo + xlen > xcap) xlen = static_cast<uint32_t>(xcap - xlo);
+        tiles.push_back({xlo, static_cast<uint16_t>(xlen), blk, static_cast<uint32_t>(segs.size()),
+                         static_cast<uint32_t>(segs.size() + (j - i))});
+        for (size_t q = i; q < j; ++q) {
+          segs.push_back({S[q].p0, S[q].n, S[q].row, S[q].slot, S[q].lane0, S[q].flags});
+          wave_nnz += S[q].n;
+          wave_rows += (S[q].flags & kSegLast) ? 1 : 0;
+        }
+        i = j;
       }
-      // longest segment first inside the tile (warps pull segments dynamically)
-      std::stable_sort(S.begin() + i, S.begin() + j,
-                       [](const HostSeg& a, const HostSeg& b) { return a.n > b.n; });
-      uint32_t xlen = (hi - xlo + 1 + align - 1) / align * align;
-      if (xlo + xlen > xcap) xlen = static_cast<uint32_t>(xcap - xlo);
-      tiles.push_back({xlo, xlen, static_cast<uint32_t>(segs.size()),
-                       static_cast<uint32_t>(segs.size() + (j - i))});
-      for (size_t k = i; k < j; ++k) {
-        segs.push_back({S[k].p0, S[k].n, S[k].row, S[k].slot, S[k].lane0, S[k].flags});
-        wave_nnz += S[k].n;
-        wave_rows += (S[k].flags & kSegLast) ? 1 : 0;
-      }
-      i = j;
+      if (w == 0) h->blk_tiles[k] = static_cast<uint32_t>(tiles.size() - tiles_before);
     }
     h->wave_tiles[w] = static_cast<uint32_t>(tiles.size());
     h->wave_nnz[w] = wave_nnz;
@@ -237,6 +261,12 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     h->plan_bytes += h->n_split_rows * 32 * h->acc_bytes;
   }
   DG_CUDA(cudaMalloc(&h->d_counters, Handle::kMaxWaves * sizeof(uint32_t)));
+  DG_CUDA(cudaMalloc(&h->d_blk_left, Handle::kMaxBlocks * sizeof(uint32_t)));
+  DG_CUDA(cudaMalloc(&h->d_blk_left_init, Handle::kMaxBlocks * sizeof(uint32_t)));
+  DG_CUDA(cudaMalloc(&h->d_blk_flag, Handle::kMaxBlocks * sizeof(uint32_t)));
+  DG_CUDA(cudaMemcpy(h->d_blk_left_init, h->blk_tiles, Handle::kMaxBlocks * sizeof(uint32_t),
+                     cudaMemcpyHostToDevice));
+  DG_CUDA(cudaMemset(h->d_blk_flag, 0, Handle::kMaxBlocks * sizeof(uint32_t)));
   return DG_OK;
 }
 

@@ -39,8 +39,20 @@ struct Segment {  // 24 bytes
 constexpr uint16_t kSegFirst = 1, kSegLast = 2, kSegGlobalX = 4;
 
 struct Tile {  // 16 bytes
-  uint32_t xlo, xlen;  // x window (16-byte aligned start, 16-byte multiple length)
+  uint32_t xlo;   // x window start (16-byte aligned)
+  uint16_t xlen;  // x window length in elements (16-byte multiple; 0: global-x tile)
+  uint16_t blk;   // output row block whose rows this tile finishes (kNoBlock: none)
   uint32_t seg0, seg1;
+};
+constexpr uint16_t kNoBlock = 0xFFFF;
+
+// Row-block completion signals: the CTA finishing the last tile of output row block k publishes
+// flag[k] = epoch, which a copy stream waits on (cuStreamWaitValue32) to move block k of d to the
+// host while the kernel still works on later blocks.  left == nullptr disables signalling.
+struct BlockSignal {
+  uint32_t* left;  // tiles still to finish per block (reset before each dose)
+  uint32_t* flag;
+  uint32_t epoch;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -357,7 +369,7 @@ template <class M, typename Acc, int WARPS, int U, int R = 0, int P = 0>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     k_tiles(M mat, const Acc* __restrict__ x, const Tile* __restrict__ tiles, uint32_t n_tiles,
             const Segment* __restrict__ segs, Acc* __restrict__ state, double* __restrict__ y,
-            uint32_t* __restrict__ counter, uint32_t wcap) {
+            uint32_t* __restrict__ counter, uint32_t wcap, BlockSignal sig) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[2];
   __shared__ uint32_t tile_of[2], seg_next[2], done[2];
@@ -441,9 +453,19 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     }
     __syncwarp();
     if (lane == 0) {
-      __threadfence_block();  // this warp's reads of buffer b happen before the count
-      if (atomicAdd(&done[b], 1u) == WARPS - 1) {
+      // this warp's reads of buffer b (and, when signalling, its d stores) happen before the count
+      if (sig.left) __threadfence(); else __threadfence_block();
+      if (atomicAdd(&done[b], 1u) == WARPS - 1) {  // the tile is finished
         __threadfence_block();
+        if (sig.left && T.blk != kNoBlock) {
+          __threadfence();
+          if (atomicSub(&sig.left[T.blk], 1u) == 1u) {
+            __threadfence();
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(sig.flag + T.blk),
+                         "r"(sig.epoch)
+                         : "memory");
+          }
+        }
         refill(b);
       }
     }

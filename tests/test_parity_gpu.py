@@ -443,3 +443,22 @@ def test_v0_warp_plan_still_bit_exact(port, golden, desk, monkeypatch):
     x = port.seeded_vector(m.cols, 42)
     assert f"{dg.checksum_bits(dg.spmv_rowchunk(to_dg(m), x)):016x}" == \
         golden["prostate-desk"]["rowchunk"]["32"]
+
+
+def test_overlapped_download_matches_device_result(monkeypatch):
+    """Host d is downloaded block by block as the tile kernel publishes row-block completion
+    (cuStreamWaitValue32 on per-block epochs); repeated doses must never read a stale block."""
+    import torch
+    p = dg.profiles.c1()
+    with dg.DoseEngine.generate(p) as e:
+        assert e.info["nnz"] > 16 << 20  # large enough for 8 output row blocks
+        yd = torch.empty(p.rows, dtype=torch.float64, device="cuda")
+        for seed in (42, 7, 8, 9):
+            x = dg.seeded_vector(p.cols, seed)
+            xd = torch.from_numpy(x).cuda()
+            e.dose_device(xd.data_ptr(), p.cols, yd.data_ptr())
+            yh = e.dose(x)  # overlapped path
+            assert np.array_equal(bits(yh), yd.cpu().numpy().view(np.uint64)), seed
+    monkeypatch.setenv("DG_NO_OVERLAP", "1")
+    with dg.DoseEngine.generate(p) as e:
+        assert np.array_equal(bits(e.dose(x)), bits(yh))
