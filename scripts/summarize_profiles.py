@@ -1,0 +1,95 @@
+"""Turn a round's gpurun_out/ evidence into committed summaries under profiles/.
+
+    python scripts/summarize_profiles.py <round-tag>      e.g. r01
+
+Reads gpurun_out/launches.csv (ncu launch list of the bench command), gpurun_out/prof_exact.ncu-rep
+and prof_fp32.ncu-rep (ncu --set full of the hot kernel) and writes:
+  profiles/<tag>_launches.txt        per-kernel launch times and share of the dose step
+  profiles/<tag>_ncu_<family>.txt    key throughput / memory / stall metrics + hottest SASS lines
+  profiles/dram_bytes_per_launch.json  DRAM read+write bytes per launch (bench.py "traffic")
+"""
+import collections
+import csv
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "gpurun_out")
+PROF = os.path.join(ROOT, "profiles")
+sys.path.insert(0, os.path.join(ROOT, "scripts"))
+
+
+def launches(tag):
+    path = os.path.join(OUT, "launches.csv")
+    rows = list(csv.reader(open(path)))
+    hdr = None
+    per = collections.OrderedDict()
+    for r in rows:
+        if r and r[0] == "ID":
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            d = dict(zip(hdr, r))
+            if d["Metric Name"] != "gpu__time_duration.sum":
+                continue
+            name = d["Kernel Name"].split("(")[0]
+            v = float(d["Metric Value"]) * (1e-3 if d["Metric Unit"] == "ns" else
+                                            1.0 if d["Metric Unit"] == "us" else 1e3)
+            per.setdefault(name, []).append(v)
+    dose = {k: v for k, v in per.items() if "gen_" not in k and "cub::" not in k and
+            "row_extents" not in k and "split_rows" not in k and "validate" not in k}
+    step = sum(sum(v) for v in dose.values()) / max(1, max(len(v) for v in dose.values()))
+    lines = [f"# {tag}: ncu launch list of `python bench.py --steps 3 --warmup 3` (C2), "
+             "gpu__time_duration.sum, --clock-control none (cold-cache, serialised launches)",
+             f"{'kernel':70s} {'launches':>8s} {'avg us':>10s} {'share of dose':>14s}"]
+    for k, v in per.items():
+        avg = sum(v) / len(v)
+        share = (sum(v) / len(v)) / step if k in dose else float("nan")
+        lines.append(f"{k[:70]:70s} {len(v):8d} {avg:10.1f} {share:14.3f}")
+    open(os.path.join(PROF, f"{tag}_launches.txt"), "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
+def ncu(tag, family):
+    rep = os.path.join(OUT, f"prof_{family}.ncu-rep")
+    if not os.path.exists(rep):
+        return None
+    summ = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "ncu_summary.py"), rep],
+                          capture_output=True, text=True).stdout
+    hot = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "ncu_sass_hot.py"), rep,
+                          "stall", "25"], capture_output=True, text=True).stdout
+    text = (f"# {tag}: ncu --set full --clock-control none, hot kernel k_tiles (C2, {family})\n"
+            + summ + "\n# hottest SASS by warp-stall samples (addr, executed, samples, instr)\n" + hot)
+    open(os.path.join(PROF, f"{tag}_ncu_{family}.txt"), "w").write(text)
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    r = list(csv.reader(raw.splitlines()))
+    hdr, units, vals = r[0], r[1], r[2]
+
+    def get(k):
+        v = float(vals[hdr.index(k)])
+        u = units[hdr.index(k)]
+        return v * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}.get(u, 1)
+
+    return get("dram__bytes_read.sum") + get("dram__bytes_write.sum")
+
+
+def main():
+    tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+    os.makedirs(PROF, exist_ok=True)
+    if os.path.exists(os.path.join(OUT, "launches.csv")):
+        launches(tag)
+    tf = os.path.join(PROF, "dram_bytes_per_launch.json")
+    traffic = json.load(open(tf)) if os.path.exists(tf) else {}
+    for fam in ("exact", "fp32"):
+        t = ncu(tag, fam)
+        if t is not None:
+            traffic[f"c2:{fam}:[w0]"] = int(t)
+            print(fam, "dram bytes per launch", t)
+    json.dump(traffic, open(tf, "w"), indent=1, sort_keys=True)
+
+
+if __name__ == "__main__":
+    main()
