@@ -174,11 +174,12 @@ void launch_group(Handle* h, int b, const char* name, cudaStream_t s, const M& m
 
 // One persistent launch per wave (one CTA per SM): wave k continues the segments whose lane
 // partials wave k-1 stored.
-template <class M, typename Acc, int kWarps, int kU, int kR = 0, int kP = 0>
+template <class M, typename Acc, int kWarps, int kU, int kR = 0, int kP = 0, int kNB = 2>
 int launch_tiles_cfg(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t s) {
-  const size_t smem = 2ull * h->window_cols * sizeof(Acc) + ring_smem_bytes<kWarps, kR>();
+  const size_t smem = static_cast<size_t>(kNB) * h->window_cols * sizeof(Acc) +
+                      ring_smem_bytes<kWarps, kR>();
   if (!h->tiles_attr) {  // a handle has one (M, Acc, config) and one device
-    DG_CUDA(cudaFuncSetAttribute(k_tiles<M, Acc, kWarps, kU, kR, kP>,
+    DG_CUDA(cudaFuncSetAttribute(k_tiles<M, Acc, kWarps, kU, kR, kP, kNB>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
     h->tiles_attr = true;
@@ -191,12 +192,13 @@ int launch_tiles_cfg(Handle* h, const M& mat, const Acc* x, double* y, cudaStrea
     sig = {h->d_blk_left, h->d_blk_flag, h->epoch};
   }
   DG_CUDA(cudaEventRecord(h->ev_tiles_start, s));  // every row not owned by a tile is final here
-  static const char* const kWaveName[] = {"[w0]", "[w1]", "[w2]", "[w3]", "[w4]", "[w5]",
-                                          "[w6]", "[w7]", "[w8+]"};
+  static const char* const kWaveName[] = {"tiles[w0]", "tiles[w1]", "tiles[w2]", "tiles[w3]",
+                                          "tiles[w4]", "tiles[w5]", "tiles[w6]", "tiles[w7]",
+                                          "tiles[w8+]"};
   for (uint32_t w = 0; w < h->n_waves; ++w) {
     if (!h->wave_tiles[w]) continue;
     const int grid = std::min<int>(h->sm_count, static_cast<int>(h->wave_tiles[w]));
-    k_tiles<M, Acc, kWarps, kU, kR, kP><<<grid, kWarps * 32, smem, s>>>(
+    k_tiles<M, Acc, kWarps, kU, kR, kP, kNB><<<grid, kWarps * 32, smem, s>>>(
         mat, x, static_cast<const Tile*>(h->d_tiles[w]), h->wave_tiles[w],
         static_cast<const Segment*>(h->d_segs[w]), static_cast<Acc*>(h->d_state), y,
         h->d_counters + w, h->window_cols, sig);
@@ -206,44 +208,53 @@ int launch_tiles_cfg(Handle* h, const M& mat, const Acc* x, double* y, cudaStrea
   return DG_OK;
 }
 
-// (warps per CTA, batch depth U) of the tile kernel; DG_TILE_CFG selects an alternative for the
-// hot (Packed16) stream when measuring.
+// Tile-kernel configurations (warps per CTA, batch depth U, TMA ring stages R, L2 prefetch
+// distance P, x-window buffers NB).  DG_TILE_CFG selects an alternative for measurement; the
+// default is the measured best on C2 (profiles/).  Config 6 is the TMA-ring variant of the matrix
+// stream (measured slower: instruction-bound), kept for A/B.
+struct TileCfg {
+  int nb;      // x-window buffers
+  bool ring;   // TMA-ring matrix stream (24 warps x 4 stages)
+};
+TileCfg tile_cfg_of(int cfg, bool packed) {
+  if (!packed) return {2, false};
+  switch (cfg) {
+    case 6: return {2, true};
+    case 12: return {3, false};
+    case 13: return {4, false};
+    default: return {2, false};
+  }
+}
+
 template <class M, typename Acc>
 int launch_tiles(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t s,
                  const char* /*name*/) {
   if (!h->n_waves) return DG_OK;
   if constexpr (std::is_same_v<M, Packed16>) {
+    constexpr int kP = std::is_same_v<Acc, float> ? 4 : 2;  // measured: prefetch distance
     switch (h->tile_cfg) {
-      case 1: return launch_tiles_cfg<M, Acc, 32, 4>(h, mat, x, y, s);
-      case 2: return launch_tiles_cfg<M, Acc, 24, 8>(h, mat, x, y, s);
-      case 3: return launch_tiles_cfg<M, Acc, 16, 16>(h, mat, x, y, s);
-      case 4: return launch_tiles_cfg<M, Acc, 32, 6>(h, mat, x, y, s);
       case 6: return launch_tiles_cfg<M, Acc, 24, 8, 4>(h, mat, x, y, s);
       case 8: return launch_tiles_cfg<M, Acc, 32, 8, 0, 1>(h, mat, x, y, s);
-      case 9: return launch_tiles_cfg<M, Acc, 32, 8, 0, 2>(h, mat, x, y, s);
       case 10: return launch_tiles_cfg<M, Acc, 32, 8, 0, 4>(h, mat, x, y, s);
       case 11: return launch_tiles_cfg<M, Acc, 32, 8, 0, 0>(h, mat, x, y, s);
-      default: break;
+      case 12: return launch_tiles_cfg<M, Acc, 32, 8, 0, kP, 3>(h, mat, x, y, s);
+      case 13: return launch_tiles_cfg<M, Acc, 32, 8, 0, kP, 4>(h, mat, x, y, s);
+      default:
+        return launch_tiles_cfg<M, Acc, Handle::kTileWarps, Handle::kTileUnroll, 0, kP>(h, mat, x,
+                                                                                       y, s);
     }
-    // measured on C2 (profiles/): L2 prefetch 2 batches ahead (exact) / 4 ahead (fp32)
-    if constexpr (std::is_same_v<Acc, float>)
-      return launch_tiles_cfg<M, Acc, Handle::kTileWarps, Handle::kTileUnroll, 0, 4>(h, mat, x, y, s);
-    else
-      return launch_tiles_cfg<M, Acc, Handle::kTileWarps, Handle::kTileUnroll, 0, 2>(h, mat, x, y, s);
   }
   return launch_tiles_cfg<M, Acc, Handle::kTileWarps, Handle::kTileUnroll>(h, mat, x, y, s);
 }
 
-// Bytes of one x-window buffer for a tile configuration: what is left of the 227 KB of shared
-// memory per CTA after the TMA rings, split in two buffers, rounded down to 1 KB.
+// Bytes of one x-window buffer: what is left of the 227 KB of shared memory per CTA after the
+// TMA rings, split in NB buffers, rounded down to 1 KB.
 uint32_t window_bytes_for(int cfg, bool packed) {
   constexpr size_t kMaxDyn = 232448 - 256;  // cudaDevAttrMaxSharedMemoryPerBlockOptin - static
-  size_t ring = 0;
-  if (packed) {
-    if (cfg == 6) ring = ring_smem_bytes<24, 4>();
-  }
-  if (!ring) return kWindowBytes;
-  return static_cast<uint32_t>(((kMaxDyn - ring) / 2) & ~size_t(1023));
+  const TileCfg c = tile_cfg_of(cfg, packed);
+  const size_t ring = c.ring ? ring_smem_bytes<24, 4>() : 0;
+  if (!ring && c.nb == 2) return kWindowBytes;
+  return static_cast<uint32_t>(((kMaxDyn - ring) / c.nb) & ~size_t(1023));
 }
 
 template <class M>
@@ -326,6 +337,8 @@ int finish_create(Handle* h, const std::vector<uint64_t>& lens) {
   h->acc_bytes = h->accumulation == DG_ACCUM_FP32 ? 4 : 8;
   if (const char* tn = std::getenv("DG_TILE_NNZ")) h->tile_nnz = std::strtoull(tn, nullptr, 10);
   if (const char* tc = std::getenv("DG_TILE_CFG")) h->tile_cfg = std::atoi(tc);
+  if (const char* gm = std::getenv("DG_GLOBAL_MIN_LEN"))
+    h->global_min_len = std::strtoull(gm, nullptr, 10);
   h->window_cols = window_bytes_for(h->tile_cfg, h->packed) / h->acc_bytes;
   DG_TRY(build_plan(h, lens));
   if (h->use_tiles) DG_TRY(plan_tiles(h, lens));

@@ -50,6 +50,7 @@ struct Handle {
   uint32_t n_waves = 0;
   uint64_t n_split_rows = 0, n_global_rows = 0;
   uint64_t short_max = 32;  // rows with len <= short_max use the sub-warp bins, others the tiles
+  uint64_t global_min_len = ~0ull;  // dense rows at least this long read x from global memory
   uint32_t wave_tiles[kMaxWaves] = {};
   uint64_t wave_nnz[kMaxWaves] = {}, wave_rows[kMaxWaves] = {};
   void* d_tiles[kMaxWaves] = {};

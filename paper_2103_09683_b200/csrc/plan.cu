@@ -101,7 +101,8 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     const uint32_t c0 = ext[r].x, c1 = ext[r].y;
     const uint64_t span = static_cast<uint64_t>(c1) - c0 + 1;
     const uint16_t whole = static_cast<uint16_t>(kSegFirst | kSegLast);
-    if (span <= ws) {
+    const bool dense_long = lens[r] >= h->global_min_len && 4 * lens[r] >= 3 * span;
+    if (span <= ws && !dense_long) {
       waves[0].push_back({rp[r], static_cast<uint32_t>(lens[r]), static_cast<uint32_t>(r), 0, c0,
                           c1, 0, whole});
     } else if (4 * lens[r] >= 3 * span) {

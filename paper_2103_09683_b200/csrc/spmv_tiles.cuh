@@ -365,14 +365,14 @@ constexpr size_t ring_smem_bytes() {
 
 // Persistent: one CTA per SM; dynamic smem = 2 * wcap * sizeof(Acc) (two x-window buffers)
 // + ring_smem_bytes<WARPS, R>() (R > 0: TMA-streamed matrix, Packed16 only).
-template <class M, typename Acc, int WARPS, int U, int R = 0, int P = 0>
+template <class M, typename Acc, int WARPS, int U, int R = 0, int P = 0, int NB = 2>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     k_tiles(M mat, const Acc* __restrict__ x, const Tile* __restrict__ tiles, uint32_t n_tiles,
             const Segment* __restrict__ segs, Acc* __restrict__ state, double* __restrict__ y,
             uint32_t* __restrict__ counter, uint32_t wcap, BlockSignal sig) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t full[2];
-  __shared__ uint32_t tile_of[2], seg_next[2], done[2];
+  __shared__ __align__(8) uint64_t full[NB];
+  __shared__ uint32_t tile_of[NB], seg_next[NB], done[NB];
   Acc* const xbuf0 = reinterpret_cast<Acc*>(smem_raw);
   const uint32_t lane = threadIdx.x & 31;
 
@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   uint64_t* my_bars = nullptr;
   uint32_t ring_parity = 0;
   if constexpr (R > 0) {
-    unsigned char* p = smem_raw + 2ull * wcap * sizeof(Acc);
+    unsigned char* p = smem_raw + static_cast<size_t>(NB) * wcap * sizeof(Acc);
     uint32_t* rings = reinterpret_cast<uint32_t*>(p);
     StageMeta* metas = reinterpret_cast<StageMeta*>(p + WARPS * R * kStageElems * 4);
     uint64_t* bars = reinterpret_cast<uint64_t*>(p + WARPS * R * kStageElems * 4 +
@@ -415,22 +415,19 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     if (lane < R) mbar_init(&my_bars[lane], 1);
   }
   if (threadIdx.x == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
+    for (int i = 0; i < NB; ++i) mbar_init(&full[i], 1);
   }
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
-  if (threadIdx.x == 0) {
-    refill(0);
-    refill(1);
-  }
+  if (threadIdx.x == 0)
+    for (int i = 0; i < NB; ++i) refill(i);
   __syncthreads();
 
-  uint32_t phase0 = 0, phase1 = 0;
+  uint32_t phases = 0;
   int b = 0;
   for (;;) {
-    if (b == 0) { mbar_wait(&full[0], phase0); phase0 ^= 1u; }
-    else        { mbar_wait(&full[1], phase1); phase1 ^= 1u; }
+    mbar_wait(&full[b], (phases >> b) & 1u);
+    phases ^= 1u << b;
     const uint32_t t = *reinterpret_cast<volatile uint32_t*>(&tile_of[b]);
     if (t >= n_tiles) break;
     const Tile T = tiles[t];
@@ -470,7 +467,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       }
     }
     __syncwarp();
-    b ^= 1;
+    b = b + 1 == NB ? 0 : b + 1;
   }
 }
 
