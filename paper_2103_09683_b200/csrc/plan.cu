@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
 #include <vector>
 
@@ -168,7 +169,9 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
   h->n_global_rows = global_x.size();
   // Output row blocks: contiguous, byte-balanced row ranges whose tiles are listed block after
   // block, so block k of d is complete (and can be downloaded) while later blocks still run.
-  const uint32_t K = h->nnz >= (16ull << 20) ? Handle::kMaxBlocks : 1;
+  uint32_t K = h->nnz >= (16ull << 20) ? Handle::kMaxBlocks : 1;
+  if (const char* kb = std::getenv("DG_BLOCKS"))
+    K = std::max<uint32_t>(1, std::min<uint32_t>(Handle::kMaxBlocks, std::atoi(kb)));
   {
     std::vector<uint64_t> b(K + 1);
     std::vector<uint32_t> l32(rows);
