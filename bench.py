@@ -58,8 +58,8 @@ def workload(cfg: str, rows_override: int = 0):
         ps = [P.c2()]
     elif cfg == "c4":
         ps = P.c4_beams()
-    else:  # c5: one scenario (the per-scenario evaluation)
-        ps = [P.c5_scenarios()[0]]
+    else:  # c5: the nine robust scenarios (separate matrices, evaluated back to back)
+        ps = P.c5_scenarios()
     if rows_override:
         for p in ps:
             p.rows = rows_override
@@ -71,7 +71,8 @@ def workload_desc(cfg, ps):
             "c2": "C2 clinical-scale synthetic DDM 8M voxels x 40k spots ~3.2e9 nnz, skewed "
                   "(configs[1])",
             "c4": "C4 6-beam hstack 2.97M voxels x 196,608 spots, U32 indices (configs[3])",
-            "c5": "C5 one robust scenario 88M voxels x 40k spots (configs[4])"}[cfg]
+            "c5": "C5 robust planning: 9 scenarios x 88M voxels x 40k spots, each GPU holds 1/8 "
+                  "of every scenario (configs[4])"}[cfg]
 
 
 def measured_hbm_peak():
@@ -130,6 +131,8 @@ def cpu_reference_run(ps, sample_rows: int, reps: int, warmup: int) -> dict:
     by oracle/Makefile): ddm::generate on a row sample of the workload's profile, then
     ddm::run_bench(RowChunk, lane_width 32, workers = all host threads) -- bench.cpp:38-103."""
     from oracle.oracle import Oracle, Profile, have_reference, traffic_bytes
+    if len(ps) > 1 and len({p.cols for p in ps}) == 1 and ps[0].seed > 100:
+        ps = ps[:1]  # C5: the scenarios are separate matrices; sample one of them
     cores = os.cpu_count() or 1
     kind = "reference" if have_reference() else "port"
     orc = Oracle(kind)
@@ -207,6 +210,37 @@ def metric_name(cfg):
 
 
 # ---------------------------------------------------------------------- our arm ------------
+def build_engines(args, dg, rank, world, local, accum):
+    """This rank's resident matrices.  C1/C2/C4: one matrix, row-sharded nnz-balanced over the
+    ranks (strong scaling).  C5: the nine robust scenarios, each cut into 8 nnz-balanced row
+    shards; rank r holds shard r of every scenario -- one GPU's share of the 8-GPU residency
+    (weak scaling: per-GPU work is fixed)."""
+    ps = workload(args.config, args.rows)
+    cols = sum(p.cols for p in ps)
+    bpn = 2 + (2 if cols < 65536 else 4)
+    engines = []
+    if args.config == "c5":
+        if world > 8:
+            raise SystemExit("c5 is laid out over 8 GPUs")
+        for p in ps:
+            lens = dg.generated_row_lengths(p, 0, p.rows, device=local)
+            b = dg.partition_lengths(lens, 8, bpn)
+            engines.append(dg.DoseEngine.generate(p, row_begin=int(b[rank]), row_end=int(b[rank + 1]),
+                                                  device=local, accumulation=accum))
+        return ps, cols, engines, None
+    rows = ps[0].rows
+    bounds = None
+    if world > 1:
+        lens = dg.generated_row_lengths(ps, 0, rows, device=local)
+        bounds = dg.partition_lengths(lens, world, bpn)
+        r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+    else:
+        r0, r1 = 0, rows
+    engines.append(dg.DoseEngine.generate(ps, row_begin=r0, row_end=r1, device=local,
+                                          accumulation=accum))
+    return ps, cols, engines, bounds
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -222,30 +256,32 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    ps = workload(args.config, args.rows)
-    rows, cols = ps[0].rows, sum(p.cols for p in ps)
     accum = dg.ACCUM_EXACT if args.accum == "exact" else dg.ACCUM_FP32
     t0 = time.time()
-    if world > 1:  # nnz-balanced contiguous row shards (8(e)), from the generator's lengths
-        lens = dg.generated_row_lengths(ps, 0, rows, device=local)
-        bounds = dg.partition_lengths(lens, world, 2 + (2 if cols < 65536 else 4))
-        r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
-    else:
-        r0, r1 = 0, rows
-    eng = dg.DoseEngine.generate(ps, row_begin=r0, row_end=r1, device=local, accumulation=accum)
+    ps, cols, engines, bounds = build_engines(args, dg, rank, world, local, accum)
     setup_s = time.time() - t0
-    info = eng.info
+    rows_total = ps[0].rows * (len(ps) if args.config == "c5" else 1)
     x_host = dg.seeded_vector(cols, 42)
     x = torch.from_numpy(x_host).cuda()
-    y = torch.empty(info["rows"], dtype=torch.float64, device="cuda")
+    ys = [torch.empty(e.info["rows"], dtype=torch.float64, device="cuda") for e in engines]
     # a real (non-legacy) stream shared by our kernels and the timing events
     torch_stream = torch.cuda.Stream()
     torch.cuda.set_stream(torch_stream)
     stream = torch_stream.cuda_stream
 
-    def step(profile=False):
-        eng.dose_device(x.data_ptr(), cols, y.data_ptr(), stream=stream, sync=False,
-                        profile=profile)
+    def step(profile=False, engs=None):
+        for e, y in zip(engs or engines, ys):
+            e.dose_device(x.data_ptr(), cols, y.data_ptr(), stream=stream, sync=False,
+                          profile=profile)
+
+    def timed(fn, n):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(n):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -253,74 +289,66 @@ def run_ours(args):
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-
     clocks = ClockSampler(local)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(args.steps):
-        step()
-    e1.record()
-    torch.cuda.synchronize()
+    ms = timed(step, args.steps)
     clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
     if dist:
         dist.barrier()
 
-    # dominant kernel, CUDA events per launch (same stream), right after the timed region
+    # dominant kernel: CUDA events per launch (same stream), right after the timed region
     prof_steps = min(args.steps, 10)
     per = {}
     for _ in range(prof_steps):
-        step(profile=True)
-        for k in eng.kernel_times():
-            d = per.setdefault(k["name"], {"ms": 0.0, "bytes": k["bytes"], "nnz": k["nnz"],
-                                           "rows": k["rows"]})
-            d["ms"] += k["ms"] / prof_steps
+        for e, y in zip(engines, ys):
+            e.dose_device(x.data_ptr(), cols, y.data_ptr(), stream=stream, sync=False, profile=True)
+            for k in e.kernel_times():
+                d = per.setdefault(k["name"], {"ms": 0.0, "bytes": 0})
+                d["ms"] += k["ms"] / prof_steps
+                d["bytes"] += k["bytes"] / prof_steps
     dom_name, dom = max(per.items(), key=lambda kv: kv[1]["ms"])
 
     # end to end through the public API: pinned host x and d, H2D + kernels + D2H timed
     e2e_steps = args.e2e_steps or min(args.steps, 10)
     xh = torch.from_numpy(x_host).pin_memory()
-    yh = torch.empty(info["rows"], dtype=torch.float64).pin_memory()
-    eng.dose_host_ptrs(xh.data_ptr(), cols, yh.data_ptr(), stream=stream)  # warm
+    yhs = [torch.empty(e.info["rows"], dtype=torch.float64).pin_memory() for e in engines]
+
+    def e2e_step(engs=None):
+        for e, yh in zip(engs or engines, yhs):
+            e.dose_host_ptrs(xh.data_ptr(), cols, yh.data_ptr(), stream=stream)
+
+    e2e_step()
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record()
-    for _ in range(e2e_steps):
-        eng.dose_host_ptrs(xh.data_ptr(), cols, yh.data_ptr(), stream=stream)
-    f1.record()
-    torch.cuda.synchronize()
-    e2e_ms = f0.elapsed_time(f1)
-    assert np.array_equal(yh.numpy().view(np.uint64), y.cpu().numpy().view(np.uint64)), \
-        "host-path d differs from device-path d"
+    e2e_ms = timed(e2e_step, e2e_steps)
+    for yh, y in zip(yhs, ys):
+        assert np.array_equal(yh.numpy().view(np.uint64), y.cpu().numpy().view(np.uint64)), \
+            "host-path d differs from device-path d"
 
-    # N > 1: the dose slices all-gathered over NCCL into the full d on every rank (8(e)),
+    # N > 1 (C2/C3): the d slices all-gathered over NCCL into the full d on every rank (8(e)),
     # timed separately from the sharded-resident step
     gather_ms = 0.0
-    if dist:
+    if dist and bounds is not None:
         from paper_2103_09683_b200.sharded import gather_dose
-        bnd = np.array([0] * (world + 1), dtype=np.uint64)
-        if world > 1:
-            bnd = bounds
         for _ in range(2):
             step()
-            gather_dose(y, bnd)
+            gather_dose(ys[0], bounds)
         torch.cuda.synchronize()
         dist.barrier()
-        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        g0.record()
-        for _ in range(e2e_steps):
-            step()
-            full = gather_dose(y, bnd)
-        g1.record()
-        torch.cuda.synchronize()
-        gather_ms = g0.elapsed_time(g1)
-        assert full.numel() == rows
+        full = [None]
 
-    model_bytes = info["model_bytes"]
+        def step_gather():
+            step()
+            full[0] = gather_dose(ys[0], bounds)
+
+        gather_ms = timed(step_gather, e2e_steps)
+        assert full[0].numel() == ps[0].rows
+
+    model_bytes = sum(e.info["model_bytes"] for e in engines)
+    nnz = sum(e.info["nnz"] for e in engines)
+    lrows = sum(e.info["rows"] for e in engines)
     vals = torch.tensor([ms, e2e_ms, gather_ms], dtype=torch.float64, device="cuda")
-    sums = torch.tensor([float(model_bytes), float(info["nnz"]), 8.0 * cols, 8.0 * info["rows"]],
+    sums = torch.tensor([float(model_bytes), float(nnz), 8.0 * cols * len(engines), 8.0 * lrows],
                         dtype=torch.float64, device="cuda")
     if dist:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
@@ -328,9 +356,11 @@ def run_ours(args):
     ms, e2e_ms, gather_ms = vals.tolist()
     total_bytes, total_nnz, h2d, d2h = sums.tolist()
     ms_step = ms / args.steps
-    e2e_step = e2e_ms / e2e_steps
+    e2e_step_ms = e2e_ms / e2e_steps
 
     if rank != 0:
+        for e in engines:
+            e.close()
         if dist:
             dist.destroy_process_group()
         return
@@ -343,6 +373,7 @@ def run_ours(args):
             traffic = json.load(open(tf)).get(f"{args.config}:{args.accum}:{dom_name}")
         except Exception:
             traffic = None
+    info = engines[0].info
     line = {
         "metric": metric_name(args.config),
         "value": total_bytes / (ms_step * 1e-3) / 1e9,
@@ -352,62 +383,54 @@ def run_ours(args):
         "warmup": max(args.warmup, 3),
         "ms_per_step": ms_step,
         "higher_is_better": True,
-        "scaling": "strong",
+        "scaling": "weak" if args.config == "c5" else "strong",
         "vs_baseline": None,
         "dtype": "f64" if accum == dg.ACCUM_EXACT else "f32",
         "data": "synthetic (row-parallel device generator, reference profile statistics)",
-        "config": {"workload": workload_desc(args.config, ps), "rows": rows, "cols": cols,
+        "config": {"workload": workload_desc(args.config, ps), "rows": rows_total, "cols": cols,
                    "nnz": int(total_nnz), "value_precision": "binary16",
                    "index_bytes": info["index_bytes"],
                    "accumulation": "exact fp64, bit-identical to ddm::spmv_rowchunk L=32"
                    if accum == dg.ACCUM_EXACT else "fp32 (tol 1e-5 * max|d|)",
-                   "parallelism": f"row-shard x{world} (nnz-balanced)",
+                   "parallelism": (f"9 scenarios x 1/8 row shard per GPU x{world}"
+                                   if args.config == "c5" else
+                                   f"row-shard x{world} (nnz-balanced)"),
                    "model_bytes_per_step": int(total_bytes), "l2": "inputs larger than L2",
                    "setup_s": round(setup_s, 2)},
-        "frac_of_8TBps": total_bytes / (ms_step * 1e-3) / 8e12,
-        "frac_of_measured_hbm": total_bytes / (ms_step * 1e-3) / 1e9 / peak,
+        "frac_of_8TBps": total_bytes / (ms_step * 1e-3) / 8e12 / world,
+        "frac_of_measured_hbm": total_bytes / (ms_step * 1e-3) / 1e9 / peak / world,
         "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "bytes_per_launch": dom["bytes"],
-                     "ms_per_launch": dom["ms"],
-                     "share_of_step": dom["ms"] / ms_step,
-                     "kernels": {k: {"ms": round(v["ms"], 4), "bytes": v["bytes"]}
+                     "traffic": traffic, "bytes_per_launch": dom["bytes"] / len(engines),
+                     "ms_per_launch": dom["ms"] / len(engines),
+                     "share_of_step": dom["ms"] / (ms / args.steps if world == 1 else ms_step),
+                     "kernels": {k: {"ms": round(v["ms"], 4), "bytes": int(v["bytes"])}
                                  for k, v in per.items()}},
-        "e2e": {"value": total_bytes / (e2e_step * 1e-3) / 1e9, "unit": "GB/s",
-                "ms_per_step": e2e_step, "h2d_bytes_per_step": int(h2d),
+        "e2e": {"value": total_bytes / (e2e_step_ms * 1e-3) / 1e9, "unit": "GB/s",
+                "ms_per_step": e2e_step_ms, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
-        "gpu_launches": int(info["n_kernels"]) * args.steps * world,
-        "ms_per_step_gathered": (gather_ms / e2e_steps) if world > 1 else None,
+        "gpu_launches": sum(int(e.info["n_kernels"]) for e in engines) * args.steps * world,
+        "ms_per_step_gathered": (gather_ms / e2e_steps) if gather_ms else None,
         "clocks": clk,
     }
-    if world == 1 and accum == dg.ACCUM_EXACT and not args.no_alt_fp32:
+    if args.config == "c5":
+        line["ms_per_scenario"] = ms_step / len(engines)
+    if world == 1 and accum == dg.ACCUM_EXACT and not args.no_alt_fp32 and args.config != "c5":
         # the north_star tolerance family on the same workload, reported beside the exact one
-        eng.close()
-        ef = dg.DoseEngine.generate(ps, device=local, accumulation=dg.ACCUM_FP32)
-        stepf = lambda: ef.dose_device(x.data_ptr(), cols, y.data_ptr(), stream=stream, sync=False)
+        for e in engines:
+            e.close()
+        _, _, fengs, _ = build_engines(args, dg, rank, world, local, dg.ACCUM_FP32)
         for _ in range(3):
-            stepf()
+            step(engs=fengs)
         torch.cuda.synchronize()
-        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        h0.record()
-        for _ in range(args.steps):
-            stepf()
-        h1.record()
-        torch.cuda.synchronize()
-        fms = h0.elapsed_time(h1) / args.steps
-        fe0, fe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ef.dose_host_ptrs(xh.data_ptr(), cols, yh.data_ptr(), stream=stream)
-        fe0.record()
-        for _ in range(e2e_steps):
-            ef.dose_host_ptrs(xh.data_ptr(), cols, yh.data_ptr(), stream=stream)
-        fe1.record()
-        torch.cuda.synchronize()
-        fe2e = fe0.elapsed_time(fe1) / e2e_steps
+        fms = timed(lambda: step(engs=fengs), args.steps) / args.steps
+        e2e_step(fengs)
+        fe2e = timed(lambda: e2e_step(fengs), e2e_steps) / e2e_steps
         line["alt_fp32"] = {"dtype": "f32", "tolerance": "per-voxel |d - d_ref| <= 1e-5 max|d_ref|",
                             "value": total_bytes / (fms * 1e-3) / 1e9, "ms_per_step": fms,
                             "frac_of_measured_hbm": total_bytes / (fms * 1e-3) / 1e9 / peak,
                             "e2e": {"value": total_bytes / (fe2e * 1e-3) / 1e9, "ms_per_step": fe2e}}
-        ef.close()
+        engines = fengs
     if world == 1 and not args.no_cpu_baseline:
         try:
             r = cpu_reference_run(ps, args.cpu_sample_rows, 5, 1)
@@ -417,7 +440,8 @@ def run_ours(args):
     else:
         line["cpu_baseline"] = None
     print(json.dumps(line), flush=True)
-    eng.close()
+    for e in engines:
+        e.close()
     if dist:
         dist.destroy_process_group()
 
