@@ -216,7 +216,7 @@ def build_engines(args, dg, rank, world, local, accum):
     shards; rank r holds shard r of every scenario -- one GPU's share of the 8-GPU residency
     (weak scaling: per-GPU work is fixed)."""
     ps = workload(args.config, args.rows)
-    cols = sum(p.cols for p in ps)
+    cols = ps[0].cols if args.config == "c5" else sum(p.cols for p in ps)  # C5: not hstacked
     bpn = 2 + (2 if cols < 65536 else 4)
     engines = []
     if args.config == "c5":

@@ -230,8 +230,8 @@ template <class M, typename Acc>
 int launch_tiles(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t s,
                  const char* /*name*/) {
   if (!h->n_waves) return DG_OK;
+  constexpr int kP = std::is_same_v<Acc, float> ? 4 : 2;  // measured: prefetch distance
   if constexpr (std::is_same_v<M, Packed16>) {
-    constexpr int kP = std::is_same_v<Acc, float> ? 4 : 2;  // measured: prefetch distance
     switch (h->tile_cfg) {
       case 6: return launch_tiles_cfg<M, Acc, 24, 8, 4>(h, mat, x, y, s);
       case 8: return launch_tiles_cfg<M, Acc, 32, 8, 0, 1>(h, mat, x, y, s);
@@ -244,7 +244,7 @@ int launch_tiles(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t 
                                                                                        y, s);
     }
   }
-  return launch_tiles_cfg<M, Acc, Handle::kTileWarps, Handle::kTileUnroll>(h, mat, x, y, s);
+  return launch_tiles_cfg<M, Acc, Handle::kTileWarps, Handle::kTileUnroll, 0, kP>(h, mat, x, y, s);
 }
 
 // Bytes of one x-window buffer: what is left of the 227 KB of shared memory per CTA after the
@@ -335,6 +335,9 @@ int finish_create(Handle* h, const std::vector<uint64_t>& lens) {
   const char* plan = std::getenv("DG_PLAN");  // "warp": v0 warp-per-row plan (A/B only)
   h->use_tiles = h->lane_width == 32 && !(plan && std::strcmp(plan, "warp") == 0);
   h->acc_bytes = h->accumulation == DG_ACCUM_FP32 ? 4 : 8;
+  // ~8 tiles per SM at least (small matrices), at most 1M nonzeros per tile (C2 sweep optimum)
+  h->tile_nnz = std::max<uint64_t>(16 * 1024, std::min<uint64_t>(1024 * 1024,
+                                                                  h->nnz / (8ull * h->sm_count)));
   if (const char* tn = std::getenv("DG_TILE_NNZ")) h->tile_nnz = std::strtoull(tn, nullptr, 10);
   if (const char* tc = std::getenv("DG_TILE_CFG")) h->tile_cfg = std::atoi(tc);
   if (const char* gm = std::getenv("DG_GLOBAL_MIN_LEN"))

@@ -156,13 +156,11 @@ __device__ __forceinline__ uint32_t load_batch(const M& mat, typename M::Raw* r,
 template <int U, int P, class M>
 __device__ __forceinline__ void prefetch_batches(const M& mat, const SegRun& s, uint32_t b,
                                                  uint32_t lane) {
-  if constexpr (P > 0 && std::is_same_v<M, Packed16>) {
-    static_assert(U == 8, "one lane per 128-byte chunk of an 8-chunk batch");
-    if (lane < 8 * P) {
-      const uint32_t rel = (b + lane / 8) * (32 * U) + (lane % 8) * 32;
-      if (rel < s.hi)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(mat.w + s.base0 + rel));
-    }
+  static_assert(U == 8, "prefetch granule is an 8-chunk (256-position) batch");
+#pragma unroll
+  for (int k = 0; k < P; ++k) {
+    const uint32_t rel = (b + k) * (32 * U);
+    if (rel < s.hi) mat.prefetch256(s.base0 + rel, lane);
   }
 }
 
