@@ -244,7 +244,8 @@ int launch_tiles(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t 
                                                                                        y, s);
     }
   }
-  return launch_tiles_cfg<M, Acc, Handle::kTileWarps, Handle::kTileUnroll, 0, kP>(h, mat, x, y, s);
+  // SoA elements take two registers each: 24 warps leave room for two U = 8 batches
+  return launch_tiles_cfg<M, Acc, 24, Handle::kTileUnroll, 0, kP>(h, mat, x, y, s);
 }
 
 // Bytes of one x-window buffer: what is left of the 227 KB of shared memory per CTA after the
