@@ -128,7 +128,12 @@ int build_plan(Handle* h, const std::vector<uint64_t>& lens) {
   }
   // Few short rows: fold them into the tiles (a warp per row, one fewer launch per bin); many:
   // sub-warp bins, G = next_pow2(len) lanes per row.
-  h->short_max = short_rows * 20 < nonempty ? 0 : 32;
+  uint64_t short_nnz = 0, all_nnz = 0;
+  for (uint64_t len : lens) {
+    all_nnz += len;
+    if (len <= 32) short_nnz += len;
+  }
+  h->short_max = (short_rows * 20 < nonempty || short_nnz * 50 < all_nnz) ? 0 : 32;
   if (const char* sm = std::getenv("DG_SHORT_MAX"))
     h->short_max = std::min<uint64_t>(32, std::strtoull(sm, nullptr, 10));
   for (uint64_t r = 0; r < lens.size(); ++r) {

@@ -193,6 +193,13 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     std::vector<Segment> segs;
     segs.reserve(waves[w].size() + (w == 0 ? global_x.size() : 0));
     uint64_t wave_nnz = 0, wave_rows = 0;
+    // later waves are smaller: keep >= ~8 tiles per SM in every wave (no single-tile tails)
+    uint64_t wnnz = 0;
+    for (const HostSeg& s : waves[w]) wnnz += s.n;
+    if (w == 0)
+      for (const HostSeg& s : global_x) wnnz += s.n;
+    const uint64_t tile_nnz = std::max<uint64_t>(
+        4096, std::min<uint64_t>(h->tile_nnz, wnnz / (8ull * h->sm_count)));
     for (uint32_t k = 0; k < K; ++k) {
       // signalled only when one wave finishes every row (else the last wave owns the rows)
       const uint16_t blk = h->n_waves == 1 ? static_cast<uint16_t>(k) : kNoBlock;
@@ -204,7 +211,7 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
       while (g < G.size()) {
         uint64_t nnz = 0;
         const uint32_t s0 = static_cast<uint32_t>(segs.size());
-        while (g < G.size() && (nnz == 0 || nnz + G[g].n <= h->tile_nnz)) {
+        while (g < G.size() && (nnz == 0 || nnz + G[g].n <= tile_nnz)) {
           const HostSeg& q = G[g++];
           segs.push_back({q.p0, q.n, q.row, 0, 0, q.flags});
           nnz += q.n;
@@ -226,7 +233,7 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
         size_t j = i;
         while (j < S.size()) {
           const uint32_t nhi = std::max(hi, S[j].chi);
-          if (j > i && (static_cast<uint64_t>(nhi) - xlo + 1 > W || nnz + S[j].n > h->tile_nnz)) break;
+          if (j > i && (static_cast<uint64_t>(nhi) - xlo + 1 > W || nnz + S[j].n > tile_nnz)) break;
           hi = nhi;
           nnz += S[j].n;
           ++j;
