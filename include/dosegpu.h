@@ -124,6 +124,16 @@ int dg_create_generated(const dg_profile* beams, uint32_t n_beams, uint32_t inde
 int dg_generated_row_lengths(const dg_profile* beams, uint32_t n_beams, uint64_t row_begin,
                              uint64_t row_end, int32_t device, uint32_t* lengths_out);
 
+/* DDM1 file -> device, streamed (ddm::read_ddm, src/io.cpp:103-168; format io.hpp:10-20).
+ * The header is checked exactly as the reference does (BadMagic, UnsupportedVersion,
+ * ValidationFailure for bad precision/index/reserved bytes or implausible sizes, TruncatedFile,
+ * ValidationFailure for trailing bytes), row pointers are read to the host, and the column and
+ * value sections are streamed in large chunks through pinned double buffers straight into device
+ * memory (the on-disk little-endian section layout IS the device SoA layout), then validated,
+ * planned and packed like dg_create.  Replaces the reference's element-at-a-time reader
+ * (~80 MB/s). */
+int dg_create_from_ddm(const char* path, const dg_options* opts, dg_handle** out);
+
 int dg_destroy(dg_handle* h);
 
 /* ---- the dose evaluation ------------------------------------------------------------------ */

@@ -145,6 +145,8 @@ class Oracle:
         self._seeded = getattr(L, p + "seeded_vector")
         self._seeded.argtypes = [U64, U64, P]
         if kind != "port":
+            L.ref_write_ddm.argtypes = [C.POINTER(_Csr), C.c_char_p]
+            L.ref_read_ddm.argtypes = [C.c_char_p, C.POINTER(_Csr)]
             self._bench = L.ref_run_bench
             self._bench.argtypes = [C.POINTER(_Csr), C.c_int, U64, U64, U64, U64, U64, P,
                                     C.POINTER(C.c_uint64)]
@@ -206,6 +208,21 @@ class Oracle:
         v = np.empty(n, dtype=np.float64)
         self._seeded(n, seed, v.ctypes.data)
         return v
+
+    def write_ddm(self, m: Csr, path: str) -> None:
+        """ddm::write_ddm (io.cpp:67-96); reference back-end only."""
+        cm = m.c()
+        rc = self.lib.ref_write_ddm(C.byref(cm), path.encode())
+        if rc:
+            raise OracleError(rc, "write_ddm")
+
+    def read_ddm_status(self, path: str) -> int:
+        """ddm::read_ddm (io.cpp:103-168): 0 or 1 + Errc of the failure."""
+        out = _Csr()
+        rc = self.lib.ref_read_ddm(path.encode(), C.byref(out))
+        if rc == 0:
+            self._free(C.byref(out))
+        return int(rc)
 
     def run_bench(self, m: Csr, algorithm: int = 1, lane_width: int = 32, workers: int = 1,
                   reps: int = 3, warmup: int = 1, vector_seed: int = 42) -> dict:

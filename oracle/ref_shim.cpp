@@ -16,6 +16,7 @@
 #include "ddm/checksum.hpp"
 #include "ddm/error.hpp"
 #include "ddm/half.hpp"
+#include "ddm/io.hpp"
 #include "ddm/matgen.hpp"
 #include "ddm/sparse.hpp"
 #include "ddm/spmv.hpp"
@@ -133,6 +134,39 @@ int ref_spmv_oracle(const or_csr* m, const double* x, uint64_t x_len, double* y)
 int ref_validate(const or_csr* m) {
   const ddm::ValidationReport r = ddm::validate(to_ddm(m));
   return r.ok ? 0 : 1 + static_cast<int>(ddm::Errc::ValidationFailure);
+}
+
+// ddm::write_ddm / ddm::read_ddm (src/io.cpp:67-168): the DDM1 container.
+int ref_write_ddm(const or_csr* m, const char* path) {
+  try {
+    ddm::write_ddm(to_ddm(m), std::filesystem::path(path));
+    return 0;
+  } catch (const ddm::Error& e) {
+    return code_of(e);
+  }
+}
+
+int ref_read_ddm(const char* path, or_csr* out) {
+  std::memset(out, 0, sizeof(*out));
+  try {
+    const ddm::CsrMatrix m = ddm::read_ddm(std::filesystem::path(path));
+    out->rows = m.rows;
+    out->cols = m.cols;
+    out->nnz = m.nnz();
+    out->precision = static_cast<int>(m.precision());
+    out->index_width = m.index_width == ddm::IndexWidth::U16 ? OR_U16 : OR_U32;
+    out->row_ptr = static_cast<uint64_t*>(std::malloc((m.rows + 1) * 8));
+    std::memcpy(out->row_ptr, m.row_ptr.data(), (m.rows + 1) * 8);
+    out->col = static_cast<uint32_t*>(std::malloc(m.nnz() * 4 + 4));
+    if (m.nnz()) std::memcpy(out->col, m.col_indices.data(), m.nnz() * 4);
+    const std::size_t vb = ddm::byte_width(m.precision());
+    out->values = std::malloc(m.nnz() * vb + 8);
+    std::visit([&](const auto& v) { if (!v.empty()) std::memcpy(out->values, v.data(), v.size() * vb); },
+               m.values.data());
+    return 0;
+  } catch (const ddm::Error& e) {
+    return code_of(e);
+  }
 }
 
 uint64_t ref_checksum_bits(const double* v, uint64_t n) {

@@ -1,0 +1,154 @@
+// ddm_io.cu -- DDM1 container -> device upload.
+//
+// The reference reads a DDM1 file element by element through std::istream (get_uint_le per
+// value, src/io.cpp:132-159, ~80 MB/s).  The format's sections are already little-endian arrays in
+// exactly the SoA layout the device uses (row_ptr u64, col u16/u32, values as bit patterns), so
+// here the column and value sections are read with large pread()s into two pinned buffers and
+// copied asynchronously to the device while the next chunk is read; dg_create then validates,
+// packs and plans the device copy.
+#include <cuda_runtime.h>
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "handle.cuh"
+
+namespace {
+
+struct Fd {
+  int fd = -1;
+  ~Fd() {
+    if (fd >= 0) close(fd);
+  }
+};
+
+bool read_all(int fd, void* dst, size_t n, off_t off) {
+  char* p = static_cast<char*>(dst);
+  while (n) {
+    const ssize_t r = pread(fd, p, n, off);
+    if (r <= 0) return false;
+    p += r;
+    off += r;
+    n -= static_cast<size_t>(r);
+  }
+  return true;
+}
+
+uint64_t le64(const unsigned char* b) {
+  uint64_t v = 0;
+  for (int i = 0; i < 8; ++i) v |= static_cast<uint64_t>(b[i]) << (8 * i);
+  return v;
+}
+
+// Stream [off, off + bytes) of the file into device memory through two pinned staging buffers.
+int stream_section(int fd, off_t off, uint64_t bytes, char* d_dst, char* pinned[2], size_t chunk,
+                   cudaStream_t s, cudaEvent_t done[2]) {
+  int buf = 0;
+  for (uint64_t pos = 0; pos < bytes; pos += chunk, buf ^= 1) {
+    const size_t n = static_cast<size_t>(std::min<uint64_t>(chunk, bytes - pos));
+    DG_CUDA(cudaEventSynchronize(done[buf]));  // the copy that last used this buffer finished
+    if (!read_all(fd, pinned[buf], n, off + static_cast<off_t>(pos))) return DG_ERR_TRUNCATED_FILE;
+    DG_CUDA(cudaMemcpyAsync(d_dst + pos, pinned[buf], n, cudaMemcpyHostToDevice, s));
+    DG_CUDA(cudaEventRecord(done[buf], s));
+  }
+  return DG_OK;
+}
+
+}  // namespace
+
+extern "C" int dg_create_from_ddm(const char* path, const dg_options* opts, dg_handle** out) {
+  if (!path || !out) return DG_ERR_INVALID_CONFIG;
+  *out = nullptr;
+  Fd f;
+  f.fd = open(path, O_RDONLY);
+  if (f.fd < 0) return DG_ERR_IO_FAILURE;
+  struct stat st {};
+  if (fstat(f.fd, &st) != 0) return DG_ERR_IO_FAILURE;
+  const uint64_t fsize = static_cast<uint64_t>(st.st_size);
+
+  // header: io.hpp:10-20, checks in read_ddm's order (io.cpp:104-130)
+  unsigned char h[32];
+  const size_t hn = static_cast<size_t>(std::min<uint64_t>(32, fsize));
+  if (hn < 4 || !read_all(f.fd, h, hn, 0)) return DG_ERR_TRUNCATED_FILE;
+  if (std::memcmp(h, "DDM1", 4) != 0) return DG_ERR_BAD_MAGIC;
+  if (hn < 5) return DG_ERR_TRUNCATED_FILE;
+  if (h[4] != 1) return DG_ERR_UNSUPPORTED_VERSION;
+  if (hn < 6) return DG_ERR_TRUNCATED_FILE;
+  if (h[5] > 2) return DG_ERR_VALIDATION_FAILURE;
+  if (hn < 7) return DG_ERR_TRUNCATED_FILE;
+  if (h[6] != 2 && h[6] != 4) return DG_ERR_VALIDATION_FAILURE;
+  if (hn < 8) return DG_ERR_TRUNCATED_FILE;
+  if (h[7] != 0) return DG_ERR_VALIDATION_FAILURE;
+  if (hn < 32) return DG_ERR_TRUNCATED_FILE;
+  const uint64_t rows = le64(h + 8), cols = le64(h + 16), nnz = le64(h + 24);
+  if (rows >= (1ull << 53) || nnz >= (1ull << 53)) return DG_ERR_VALIDATION_FAILURE;
+  const uint32_t ib = h[6], vb = h[5] == 0 ? 2 : h[5] == 1 ? 4 : 8;
+  const uint64_t rp_off = 32, col_off = rp_off + 8 * (rows + 1), val_off = col_off + ib * nnz,
+                 end = val_off + vb * nnz;
+  if (fsize < end) return DG_ERR_TRUNCATED_FILE;
+  if (fsize > end) return DG_ERR_VALIDATION_FAILURE;  // trailing bytes (io.cpp:162-163)
+
+  int dev = 0;
+  DG_TRY(dg::select_device(opts ? opts->device : -1, &dev));
+  std::vector<uint64_t> rp(rows + 1);
+  if (!read_all(f.fd, rp.data(), 8 * (rows + 1), static_cast<off_t>(rp_off)))
+    return DG_ERR_TRUNCATED_FILE;
+
+  // device staging of the three sections, then the regular create path on a device view
+  uint64_t* d_rp = nullptr;
+  char *d_col = nullptr, *d_val = nullptr, *pinned[2] = {nullptr, nullptr};
+  cudaStream_t s = nullptr;
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  const size_t chunk = 64ull << 20;
+  int rc = DG_OK;
+  auto cu = [&](cudaError_t e) { if (rc == DG_OK && e != cudaSuccess) rc = DG_ERR_CUDA_BASE + (int)e; };
+  cu(cudaMalloc(&d_rp, 8 * (rows + 1)));
+  cu(cudaMalloc(&d_col, std::max<uint64_t>(ib * nnz, 16)));
+  cu(cudaMalloc(&d_val, std::max<uint64_t>(vb * nnz, 16)));
+  cu(cudaHostAlloc(&pinned[0], chunk, cudaHostAllocDefault));
+  cu(cudaHostAlloc(&pinned[1], chunk, cudaHostAllocDefault));
+  cu(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  cu(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
+  cu(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
+  if (rc == DG_OK) {
+    cu(cudaEventRecord(done[0], s));
+    cu(cudaEventRecord(done[1], s));
+    cu(cudaMemcpyAsync(d_rp, rp.data(), 8 * (rows + 1), cudaMemcpyHostToDevice, s));
+  }
+  if (rc == DG_OK) rc = stream_section(f.fd, static_cast<off_t>(col_off), ib * nnz, d_col, pinned, chunk, s, done);
+  if (rc == DG_OK) rc = stream_section(f.fd, static_cast<off_t>(val_off), vb * nnz, d_val, pinned, chunk, s, done);
+  if (rc == DG_OK) cu(cudaStreamSynchronize(s));
+  if (rc == DG_OK) {
+    dg_csr_view v{};
+    v.rows = rows;
+    v.cols = cols;
+    v.nnz = nnz;
+    v.value_precision = h[5];
+    v.index_bytes = static_cast<uint8_t>(ib);
+    v.col_storage_bytes = static_cast<uint8_t>(ib);
+    v.on_device = 1;
+    v.row_ptr = d_rp;
+    v.col_indices = d_col;
+    v.values = d_val;
+    dg_options o;
+    dg_default_options(&o);
+    if (opts) o = *opts;
+    o.device = dev;
+    rc = dg_create(&v, &o, out);
+  }
+  if (s) cudaStreamSynchronize(s);
+  cudaFree(d_rp);
+  cudaFree(d_col);
+  cudaFree(d_val);
+  cudaFreeHost(pinned[0]);
+  cudaFreeHost(pinned[1]);
+  for (auto e : done)
+    if (e) cudaEventDestroy(e);
+  if (s) cudaStreamDestroy(s);
+  return rc;
+}

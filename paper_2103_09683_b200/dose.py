@@ -117,6 +117,7 @@ _SIGS = {
                                       C.POINTER(_Options), C.POINTER(C.c_void_p)]),
     "dg_generated_row_lengths": (C.c_int, [C.POINTER(_Profile), C.c_uint32, C.c_uint64,
                                            C.c_uint64, C.c_int32, C.c_void_p]),
+    "dg_create_from_ddm": (C.c_int, [C.c_char_p, C.POINTER(_Options), C.POINTER(C.c_void_p)]),
     "dg_destroy": (C.c_int, [C.c_void_p]),
     "dg_dose": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint32, C.c_void_p]),
     "dg_get_info": (C.c_int, [C.c_void_p, C.POINTER(_Info)]),
@@ -255,6 +256,16 @@ class DoseEngine:
                         kw.get("accumulation", ACCUM_EXACT), kw.get("row_begin", 0),
                         kw.get("row_end", 0))
         _check(_lib().dg_create(C.byref(view), C.byref(opts), C.byref(h)), "dg_create")
+        return cls(h)
+
+    @classmethod
+    def from_ddm(cls, path: str, *, lane_width: int = 32, accumulation: int = ACCUM_EXACT,
+                 device: int = -1, row_begin: int = 0, row_end: int = 0) -> "DoseEngine":
+        """A DDM1 file (ddm::read_ddm's container) streamed straight into device memory."""
+        h = C.c_void_p()
+        opts = _options(device, lane_width, accumulation, row_begin, row_end)
+        _check(_lib().dg_create_from_ddm(os.fsencode(path), C.byref(opts), C.byref(h)),
+               "dg_create_from_ddm")
         return cls(h)
 
     @classmethod
