@@ -218,3 +218,28 @@ int ref_run_bench(const or_csr* m, int algorithm, uint64_t lane_width, uint64_t 
 }
 
 }  // extern "C"
+
+// ddm::render_csv (bench.cpp:141-153) of one report, for format parity of the GPU rows.
+extern "C" int ref_render_csv_row(const char* label, int algorithm, int precision, uint64_t lane,
+                                  uint64_t chunks, uint64_t workers, uint64_t reps, double mean,
+                                  double mn, double gflops, double gbps, double oi,
+                                  uint64_t checksum, char* out, uint64_t cap) {
+  ddm::BenchReport r;
+  r.matrix_label = label;
+  r.algorithm = static_cast<ddm::Algorithm>(algorithm);
+  r.precision = static_cast<ddm::ValuePrecision>(precision);
+  r.lane_width = lane;
+  r.chunk_count = chunks;
+  r.workers = workers;
+  r.repetitions = reps;
+  r.mean_seconds = mean;
+  r.min_seconds = mn;
+  r.gflops = gflops;
+  r.effective_gbps = gbps;
+  r.operational_intensity = oi;
+  r.output_checksum = checksum;
+  const std::string s = ddm::render_csv(std::span<const ddm::BenchReport>(&r, 1));
+  if (s.size() + 1 > cap) return -1;
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return 0;
+}
