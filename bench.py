@@ -45,6 +45,7 @@ def parse_args():
     ap.add_argument("--rows", type=int, default=0, help="override rows (testing)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-alt-fp32", action="store_true", help="skip the fp32-family side line")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--cpu-sample-rows", type=int, default=250_000)
     ap.add_argument("--e2e-steps", type=int, default=0, help="default: min(steps, 10)")
     return ap.parse_args()
@@ -250,11 +251,18 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # DG_BENCH_ONE_DEVICE=1 (+ --dist-backend gloo): every rank on cuda:0 -- exercises the N > 1
+    # orchestration on a single-GPU box; the timing is then not a scaling measurement
+    if os.environ.get("DG_BENCH_ONE_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(args.dist_backend)
 
     accum = dg.ACCUM_EXACT if args.accum == "exact" else dg.ACCUM_FP32
     t0 = time.time()
