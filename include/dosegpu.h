@@ -149,6 +149,21 @@ enum {
 int dg_dose(dg_handle* h, const double* x, uint64_t x_len, double* y, uint32_t flags,
             void* stream);
 
+/* ---- the column-scatter comparator --------------------------------------- */
+/* ddm::spmv_scatter_baseline (src/spmv.cpp:113-150) -- the paper's "GPU Baseline" (a CSC column
+ * scatter) done atomic-free and deterministic: columns are split into
+ * chunk_count static ranges (boundary c = cols*c/chunk_count); one CTA scatters a chunk into its
+ * private scratch vector in column-major order (one barrier per column orders the updates of a
+ * row), and the scratches are merged in chunk order.  d is bit-identical to the reference engine
+ * for the same chunk_count.  The CSC copy is built on the device (stable by row, like
+ * ddm::csr_to_csc, sparse.cpp:166-195); nnz must be < 2^31. */
+typedef struct dg_scatter dg_scatter;
+int dg_scatter_create(const dg_csr_view* view, uint32_t chunk_count, int32_t device,
+                      dg_scatter** out);
+int dg_scatter_dose(dg_scatter* s, const double* x, uint64_t x_len, double* y, uint32_t flags,
+                    void* stream);
+int dg_scatter_destroy(dg_scatter* s);
+
 /* ---- introspection ------------------------------------------------------------------------ */
 typedef struct {
   uint64_t rows, cols, nnz;          /* of the shard */

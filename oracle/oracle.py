@@ -209,6 +209,18 @@ class Oracle:
         self._seeded(n, seed, v.ctypes.data)
         return v
 
+    def spmv_scatter(self, m: Csr, x: np.ndarray, chunk_count: int = 1, workers: int = 1) -> np.ndarray:
+        """ddm::spmv_scatter_baseline on csr_to_csc(m) (spmv.cpp:113-150); reference only."""
+        f = self.lib.ref_spmv_scatter
+        f.argtypes = [C.POINTER(_Csr), C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p]
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.zeros(m.rows, dtype=np.float64)
+        cm = m.c()
+        rc = f(C.byref(cm), x.ctypes.data, len(x), chunk_count, workers, y.ctypes.data)
+        if rc:
+            raise OracleError(rc, "spmv_scatter")
+        return y
+
     def write_ddm(self, m: Csr, path: str) -> None:
         """ddm::write_ddm (io.cpp:67-96); reference back-end only."""
         cm = m.c()

@@ -243,3 +243,17 @@ extern "C" int ref_render_csv_row(const char* label, int algorithm, int precisio
   std::memcpy(out, s.c_str(), s.size() + 1);
   return 0;
 }
+
+// ddm::csr_to_csc + ddm::spmv_scatter_baseline (sparse.cpp:166-195, spmv.cpp:113-150).
+extern "C" int ref_spmv_scatter(const or_csr* m, const double* x, uint64_t x_len,
+                                uint64_t chunk_count, uint64_t workers, double* y) {
+  try {
+    const ddm::CscMatrix csc = ddm::csr_to_csc(to_ddm(m));
+    const ddm::DenseVector out = ddm::spmv_scatter_baseline(
+        csc, ddm::DenseVector(x, x + x_len), {.chunk_count = chunk_count, .workers = workers});
+    std::memcpy(y, out.data(), out.size() * 8);
+    return 0;
+  } catch (const ddm::Error& e) {
+    return code_of(e);
+  }
+}

@@ -119,6 +119,10 @@ _SIGS = {
                                            C.c_uint64, C.c_int32, C.c_void_p]),
     "dg_create_from_ddm": (C.c_int, [C.c_char_p, C.POINTER(_Options), C.POINTER(C.c_void_p)]),
     "dg_destroy": (C.c_int, [C.c_void_p]),
+    "dg_scatter_create": (C.c_int, [C.POINTER(_View), C.c_uint32, C.c_int32, C.POINTER(C.c_void_p)]),
+    "dg_scatter_dose": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint32,
+                                  C.c_void_p]),
+    "dg_scatter_destroy": (C.c_int, [C.c_void_p]),
     "dg_dose": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint32, C.c_void_p]),
     "dg_get_info": (C.c_int, [C.c_void_p, C.POINTER(_Info)]),
     "dg_last_timing": (C.c_int, [C.c_void_p, C.POINTER(_Timing)]),
@@ -350,6 +354,56 @@ class DoseEngine:
 
     def __exit__(self, *a):
         self.close()
+
+
+class ScatterEngine:
+    """The column-scatter comparator (ddm::spmv_scatter_baseline, spmv.cpp:113-150) on the GPU:
+    atomic-free, bit-identical to the reference for the same chunk_count."""
+
+    def __init__(self, m: CsrMatrix, chunk_count: int = 1, *, device: int = -1):
+        rp = np.ascontiguousarray(m.row_ptr, dtype=np.uint64)
+        col = np.ascontiguousarray(m.col_indices, dtype=np.uint32)
+        val = np.ascontiguousarray(m.values, dtype=_VDTYPE[m.precision])
+        view = _View(m.rows, m.cols, m.nnz, m.precision, 2 if m.index_width == U16 else 4, 4, 0,
+                     rp.ctypes.data, col.ctypes.data, val.ctypes.data)
+        self._h = C.c_void_p()
+        self.rows, self.cols = m.rows, m.cols
+        _check(_lib().dg_scatter_create(C.byref(view), chunk_count, device, C.byref(self._h)),
+               "dg_scatter_create")
+
+    def dose(self, x: np.ndarray) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.empty(self.rows, dtype=np.float64)
+        _check(_lib().dg_scatter_dose(self._h, x.ctypes.data, len(x), y.ctypes.data, 0, None),
+               "dg_scatter_dose")
+        return y
+
+    def dose_device(self, x_ptr: int, x_len: int, y_ptr: int, stream: int = 0) -> None:
+        _check(_lib().dg_scatter_dose(self._h, C.c_void_p(x_ptr), x_len, C.c_void_p(y_ptr),
+                                      X_ON_DEVICE | Y_ON_DEVICE | NO_SYNC,
+                                      C.c_void_p(stream) if stream else None), "dg_scatter_dose")
+
+    def close(self):
+        if self._h:
+            _lib().dg_scatter_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def spmv_scatter_baseline(m: CsrMatrix, x: np.ndarray, chunk_count: int = 1, workers: int = 1,
+                          *, device: int = -1) -> np.ndarray:
+    """ddm::spmv_scatter_baseline semantics on the GPU (the CSC is built on the device)."""
+    if len(x) != m.cols:
+        raise Error(1 + Errc.DimensionMismatch, f"input vector length {len(x)} != {m.cols}")
+    if chunk_count < 1 or workers < 1:
+        raise Error(1 + Errc.InvalidConfig, "chunk_count and workers must be >= 1")
+    with ScatterEngine(m, chunk_count, device=device) as e:
+        return e.dose(x)
 
 
 # ---------------------------------------------------------------- drop-in functions -------
