@@ -62,11 +62,15 @@ struct SoA {
   __device__ __forceinline__ static Raw filler(uint32_t col) { return {static_cast<I>(col), V(0)}; }
   // L2 prefetch of the 128-byte lines of 256 positions starting at p: lanes [0, lc) take the
   // column lines, lanes [lc, lc + lv) the value lines
-  __device__ __forceinline__ void prefetch256(uint64_t p, uint32_t lane) const {
+  __device__ __forceinline__ void prefetch256(uint64_t p, uint32_t room, uint32_t lane) const {
     constexpr uint32_t lc = 2 * sizeof(I), lv = 2 * sizeof(V);
     const char* a = nullptr;
-    if (lane < lc) a = reinterpret_cast<const char*>(col + p) + 128 * lane;
-    else if (lane < lc + lv) a = reinterpret_cast<const char*>(val + p) + 128 * (lane - lc);
+    if (lane < lc) {
+      if (lane * (128 / sizeof(I)) < room) a = reinterpret_cast<const char*>(col + p) + 128 * lane;
+    } else if (lane < lc + lv) {
+      if ((lane - lc) * (128 / sizeof(V)) < room)
+        a = reinterpret_cast<const char*>(val + p) + 128 * (lane - lc);
+    }
     if (a) asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
   }
 };
@@ -84,8 +88,9 @@ struct Packed16 {
   __device__ __forceinline__ static uint16_t c_of(Raw r) { return static_cast<uint16_t>(r >> 16); }
   __device__ __forceinline__ static uint16_t v_of(Raw r) { return static_cast<uint16_t>(r & 0xFFFFu); }
   __device__ __forceinline__ static Raw filler(uint32_t col) { return col << 16; }
-  __device__ __forceinline__ void prefetch256(uint64_t p, uint32_t lane) const {
-    if (lane < 8) asm volatile("prefetch.global.L2 [%0];" ::"l"(w + p + 32 * lane));
+  // lines of positions [p, p + min(256, room)): no line past the segment is fetched
+  __device__ __forceinline__ void prefetch256(uint64_t p, uint32_t room, uint32_t lane) const {
+    if (lane < 8 && 32 * lane < room) asm volatile("prefetch.global.L2 [%0];" ::"l"(w + p + 32 * lane));
   }
 };
 

@@ -160,7 +160,7 @@ __device__ __forceinline__ void prefetch_batches(const M& mat, const SegRun& s, 
 #pragma unroll
   for (int k = 0; k < P; ++k) {
     const uint32_t rel = (b + k) * (32 * U);
-    if (rel < s.hi) mat.prefetch256(s.base0 + rel, lane);
+    if (rel < s.hi) mat.prefetch256(s.base0 + rel, s.hi - rel, lane);
   }
 }
 
