@@ -149,6 +149,22 @@ enum {
 int dg_dose(dg_handle* h, const double* x, uint64_t x_len, double* y, uint32_t flags,
             void* stream);
 
+/* ---- fused d gather over NVLink peer memory ------------------------------- */
+/* With n targets set, every dg_dose of this (shard) handle also writes its rows straight into
+ * each target -- the full-d buffers of all ranks (this rank's included), mapped into this
+ * process through CUDA IPC (dg_ipc_*) -- at global row row_begin + r: the dose kernels' epilogues
+ * store each finished row to every target (P2P stores over NVLink, overlapped with the rest of
+ * the kernel), and this shard's row range of every target is zero-filled first (its empty rows).
+ * When every rank's dose has completed (the caller's barrier), every rank holds the full d: the
+ * all-gather costs no separate collective.  targets == NULL / n == 0 disables. */
+int dg_set_gather_targets(dg_handle* h, double* const* targets, uint32_t n);
+
+/* Minimal CUDA IPC plumbing for the targets (64-byte cudaIpcMemHandle_t). */
+int dg_ipc_alloc(uint64_t bytes, int32_t device, void** dptr, void* handle64);
+int dg_ipc_open(const void* handle64, int32_t device, void** dptr);
+int dg_ipc_close(void* dptr);
+int dg_ipc_free(void* dptr);
+
 /* ---- the column-scatter comparator --------------------------------------- */
 /* ddm::spmv_scatter_baseline (src/spmv.cpp:113-150) -- the paper's "GPU Baseline" (a CSC column
  * scatter) done atomic-free and deterministic: columns are split into

@@ -4,7 +4,7 @@ The compute lives in ``libdosegpu.so`` (hand-written sm_100a CUDA behind the C A
 include/dosegpu.h); this package is the host-side mirror of the reference's dose API.
 """
 from .dose import (ACCUM_EXACT, ACCUM_FP32, DOUBLE, HALF, SINGLE, U16, U32, CsrMatrix,
-                   DoseEngine, Errc, Error, Profile, RowChunkConfig, checksum_bits,
+                   DoseEngine, Errc, Error, PeerBuffer, Profile, RowChunkConfig, checksum_bits,
                    checksum_bits_device, exported_symbols, generated_row_lengths,
                    partition_lengths, partition_rows, seeded_vector, spmv_oracle, spmv_rowchunk,
                    traffic_bytes)
@@ -12,7 +12,7 @@ from . import profiles
 
 __all__ = [
     "ACCUM_EXACT", "ACCUM_FP32", "DOUBLE", "HALF", "SINGLE", "U16", "U32", "CsrMatrix",
-    "DoseEngine", "Errc", "Error", "Profile", "RowChunkConfig", "checksum_bits",
+    "DoseEngine", "Errc", "Error", "PeerBuffer", "Profile", "RowChunkConfig", "checksum_bits",
     "checksum_bits_device", "exported_symbols", "generated_row_lengths", "partition_lengths",
     "partition_rows", "seeded_vector", "spmv_oracle", "spmv_rowchunk", "traffic_bytes", "profiles",
 ]

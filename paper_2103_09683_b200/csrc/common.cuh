@@ -94,6 +94,18 @@ struct Packed16 {
   }
 };
 
+// Fused d gather (dg_set_gather_targets): each finished row is also stored into every rank's
+// full-d buffer (peer memory over NVLink) at its global row.
+constexpr uint32_t kMaxGatherTargets = 8;
+struct GatherTargets {
+  double* t[kMaxGatherTargets];
+  uint32_t n;
+  uint64_t row_off;
+  __device__ __forceinline__ void store(uint64_t row, double v) const {
+    for (uint32_t i = 0; i < n; ++i) t[i][row_off + row] = v;
+  }
+};
+
 __device__ __forceinline__ uint32_t pack16(uint16_t col, uint16_t half_bits) {
   return (static_cast<uint32_t>(col) << 16) | half_bits;
 }

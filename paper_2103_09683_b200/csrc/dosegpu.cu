@@ -173,7 +173,7 @@ void launch_group(Handle* h, int b, const char* name, cudaStream_t s, const M& m
   const uint32_t cnt = h->bin_count[b];
   if (!cnt) return;
   k_group<G, M, Acc><<<grid_for(static_cast<uint64_t>(cnt) * G, 256), 256, 0, s>>>(
-      mat, h->d_row_ptr, x, h->d_bin[b], cnt, y);
+      mat, h->d_row_ptr, x, h->d_bin[b], cnt, y, h->gt);
   h->post(s, name, cnt, h->bin_nnz[b]);
 }
 
@@ -206,7 +206,7 @@ int launch_tiles_cfg(Handle* h, const M& mat, const Acc* x, double* y, cudaStrea
     k_tiles<M, Acc, kWarps, kU, kR, kP, kNB><<<grid, kWarps * 32, smem, s>>>(
         mat, x, static_cast<const Tile*>(h->d_tiles[w]), h->wave_tiles[w],
         static_cast<const Segment*>(h->d_segs[w]), static_cast<Acc*>(h->d_state), y,
-        h->d_counters + w, h->window_cols, sig);
+        h->d_counters + w, h->window_cols, sig, h->gt);
     h->post(s, kWaveName[std::min<uint32_t>(w, 8)], h->wave_rows[w], h->wave_nnz[w]);
   }
   DG_CUDA(cudaGetLastError());
@@ -274,7 +274,7 @@ int launch_exact(Handle* h, const M& mat, const double* x, double* y, cudaStream
     launch_group<32>(h, 5, "group<32>", s, mat, x, y);
     if (h->bin_count[kBinLong]) {
       k_warp<M, double><<<grid_for(32ull * h->bin_count[kBinLong], 256), 256, 0, s>>>(
-          mat, h->d_row_ptr, x, h->d_bin[kBinLong], h->bin_count[kBinLong], y);
+          mat, h->d_row_ptr, x, h->d_bin[kBinLong], h->bin_count[kBinLong], y, h->gt);
       h->post(s, "warp_v0", h->bin_count[kBinLong], h->bin_nnz[kBinLong]);
     }
     DG_TRY(launch_tiles(h, mat, x, y, s, "tiles"));
@@ -290,7 +290,7 @@ int launch_exact(Handle* h, const M& mat, const double* x, double* y, cudaStream
         const uint32_t cnt = h->bin_count[kBinGeneral];
         if (cnt) {
           k_block_exact<M><<<grid_for(cnt, 1, 16), L, L * sizeof(double), s>>>(
-              mat, h->d_row_ptr, x, h->d_bin[kBinGeneral], cnt, y);
+              mat, h->d_row_ptr, x, h->d_bin[kBinGeneral], cnt, y, h->gt);
           h->post(s, "block<L>", cnt, h->bin_nnz[kBinGeneral]);
         }
       }
@@ -310,7 +310,7 @@ int launch_fp32(Handle* h, const M& mat, const float* x, double* y, cudaStream_t
   launch_group<32>(h, 5, "group_f32<32>", s, mat, x, y);
   if (h->bin_count[kBinLong]) {
     k_warp<M, float><<<grid_for(32ull * h->bin_count[kBinLong], 256), 256, 0, s>>>(
-        mat, h->d_row_ptr, x, h->d_bin[kBinLong], h->bin_count[kBinLong], y);
+        mat, h->d_row_ptr, x, h->d_bin[kBinLong], h->bin_count[kBinLong], y, h->gt);
     h->post(s, "warp_f32_v0", h->bin_count[kBinLong], h->bin_nnz[kBinLong]);
   }
   DG_TRY(launch_tiles(h, mat, x, y, s, "tiles_f32"));
@@ -321,6 +321,10 @@ int launch_fp32(Handle* h, const M& mat, const float* x, double* y, cudaStream_t
 int run_kernels(Handle* h, const double* d_x, double* d_y, cudaStream_t s) {
   h->n_launch = 0;
   if (h->rows) DG_CUDA(cudaMemsetAsync(d_y, 0, h->rows * sizeof(double), s));
+  // fused gather: this shard's rows of every rank's full d start at +0.0 (its empty rows); the
+  // kernels then store each finished row into every target over NVLink
+  for (uint32_t i = 0; i < h->gt.n && h->rows; ++i)
+    DG_CUDA(cudaMemsetAsync(h->gt.t[i] + h->gt.row_off, 0, h->rows * sizeof(double), s));
   if (h->profiling) DG_CUDA(cudaEventRecord(h->kev[0], s));
   int st;
   if (h->accumulation == DG_ACCUM_FP32) {

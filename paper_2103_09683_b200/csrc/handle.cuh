@@ -75,6 +75,9 @@ struct Handle {
   cudaEvent_t ev_tiles_start = nullptr, ev_d2h_done = nullptr;
   bool signal_blocks = false;  // this dose publishes block completion (host d, overlapped D2H)
 
+  // fused d gather: every finished row also goes to each rank's full-d buffer (peer memory)
+  GatherTargets gt = {};
+
   // staging for host x / y and the fp32 family
   double* d_x = nullptr;
   double* d_y = nullptr;

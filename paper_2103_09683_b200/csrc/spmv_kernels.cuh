@@ -40,7 +40,8 @@ template <int G, class M, typename Acc>
 __global__ void __launch_bounds__(256) k_group(M mat, const uint64_t* __restrict__ rp,
                                                const Acc* __restrict__ x,
                                                const uint32_t* __restrict__ rows,
-                                               uint32_t n_rows, double* __restrict__ y) {
+                                               uint32_t n_rows, double* __restrict__ y,
+                                               GatherTargets gt) {
   using Ops = AccOps<Acc>;
   const uint32_t lane = threadIdx.x & (G - 1);
   const uint64_t group = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / G;
@@ -59,7 +60,10 @@ __global__ void __launch_bounds__(256) k_group(M mat, const uint64_t* __restrict
     }
 #pragma unroll
     for (int w = G / 2; w >= 1; w /= 2) acc = Ops::add(acc, __shfl_down_sync(kFull, acc, w, G));
-    if (live && lane == 0) y[r] = static_cast<double>(acc);
+    if (live && lane == 0) {
+      y[r] = static_cast<double>(acc);
+      gt.store(r, static_cast<double>(acc));
+    }
   }
 }
 
@@ -69,7 +73,7 @@ template <class M, typename Acc>
 __global__ void __launch_bounds__(256) k_warp(M mat, const uint64_t* __restrict__ rp,
                                               const Acc* __restrict__ x,
                                               const uint32_t* __restrict__ rows, uint32_t n_rows,
-                                              double* __restrict__ y) {
+                                              double* __restrict__ y, GatherTargets gt) {
   using Ops = AccOps<Acc>;
   constexpr int U = 8;
   const uint32_t lane = threadIdx.x & 31;
@@ -96,7 +100,10 @@ __global__ void __launch_bounds__(256) k_warp(M mat, const uint64_t* __restrict_
     }
 #pragma unroll
     for (int off = 16; off >= 1; off /= 2) acc = Ops::add(acc, __shfl_down_sync(kFull, acc, off));
-    if (lane == 0) y[r] = static_cast<double>(acc);
+    if (lane == 0) {
+      y[r] = static_cast<double>(acc);
+      gt.store(r, static_cast<double>(acc));
+    }
   }
 }
 
@@ -105,7 +112,7 @@ __global__ void __launch_bounds__(256) k_warp(M mat, const uint64_t* __restrict_
 template <class M>
 __global__ void k_block_exact(M mat, const uint64_t* __restrict__ rp, const double* __restrict__ x,
                               const uint32_t* __restrict__ rows, uint32_t n_rows,
-                              double* __restrict__ y) {
+                              double* __restrict__ y, GatherTargets gt) {
   extern __shared__ double partial[];
   const uint32_t L = blockDim.x, l = threadIdx.x;
   for (uint32_t b = blockIdx.x; b < n_rows; b += gridDim.x) {
@@ -122,7 +129,10 @@ __global__ void k_block_exact(M mat, const uint64_t* __restrict__ rp, const doub
       if (l < w) partial[l] = __dadd_rn(partial[l], partial[l + w]);
       __syncthreads();
     }
-    if (l == 0) y[r] = partial[0];
+    if (l == 0) {
+      y[r] = partial[0];
+      gt.store(r, partial[0]);
+    }
     __syncthreads();
   }
 }

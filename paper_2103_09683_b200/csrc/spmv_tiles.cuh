@@ -193,7 +193,7 @@ template <int U, int P, class M, typename Acc, class GrabFn>
 __device__ __forceinline__ void run_segments(const M& mat, const XWindow<Acc>& xw,
                                              const XGlobal<Acc>& xg, GrabFn&& grab,
                                              Acc* __restrict__ state, double* __restrict__ y,
-                                             uint32_t lane) {
+                                             const GatherTargets& gt, uint32_t lane) {
   using Ops = AccOps<Acc>;
   using Raw = typename M::Raw;
   Segment sd;
@@ -229,7 +229,10 @@ __device__ __forceinline__ void run_segments(const M& mat, const XWindow<Acc>& x
     if (cur.flags & kSegLast) {
 #pragma unroll
       for (int off = 16; off >= 1; off /= 2) acc = Ops::add(acc, __shfl_down_sync(kFull, acc, off));
-      if (lane == 0) y[cur.row] = static_cast<double>(acc);
+      if (lane == 0) {
+        y[cur.row] = static_cast<double>(acc);
+        gt.store(cur.row, static_cast<double>(acc));
+      }
     } else {
       state[static_cast<uint64_t>(cur.slot) * 32 + lane] = acc;
     }
@@ -262,6 +265,7 @@ template <int U, int R, typename Acc, class GrabFn>
 __device__ __forceinline__ void run_segments_tma(const Packed16& mat, const XWindow<Acc>& xw,
                                                  const XGlobal<Acc>& xg, GrabFn&& grab,
                                                  Acc* __restrict__ state, double* __restrict__ y,
+                                                 const GatherTargets& gt,
                                                  uint32_t lane, uint32_t* ring, StageMeta* meta,
                                                  uint64_t* bars, uint32_t& parity) {
   static_assert(U * 32 == 256, "stage layout assumes 256-position batches");
@@ -343,7 +347,10 @@ __device__ __forceinline__ void run_segments_tma(const Packed16& mat, const XWin
       if (m.flags & kSegLast) {
 #pragma unroll
         for (int off = 16; off >= 1; off /= 2) acc = Ops::add(acc, __shfl_down_sync(kFull, acc, off));
-        if (lane == 0) y[m.row] = static_cast<double>(acc);
+        if (lane == 0) {
+          y[m.row] = static_cast<double>(acc);
+          gt.store(m.row, static_cast<double>(acc));
+        }
       } else {
         state[static_cast<uint64_t>(m.slot) * 32 + lane] = acc;
       }
@@ -367,7 +374,7 @@ template <class M, typename Acc, int WARPS, int U, int R = 0, int P = 0, int NB 
 __global__ void __launch_bounds__(WARPS * 32, 1)
     k_tiles(M mat, const Acc* __restrict__ x, const Tile* __restrict__ tiles, uint32_t n_tiles,
             const Segment* __restrict__ segs, Acc* __restrict__ state, double* __restrict__ y,
-            uint32_t* __restrict__ counter, uint32_t wcap, BlockSignal sig) {
+            uint32_t* __restrict__ counter, uint32_t wcap, BlockSignal sig, GatherTargets gt) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[NB];
   __shared__ uint32_t tile_of[NB], seg_next[NB], done[NB];
@@ -441,10 +448,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       return true;
     };
     if constexpr (R > 0) {
-      run_segments_tma<U, R>(mat, xw, xg, grab, state, y, lane, my_ring, my_meta, my_bars,
+      run_segments_tma<U, R>(mat, xw, xg, grab, state, y, gt, lane, my_ring, my_meta, my_bars,
                              ring_parity);
     } else {
-      run_segments<U, P>(mat, xw, xg, grab, state, y, lane);
+      run_segments<U, P>(mat, xw, xg, grab, state, y, gt, lane);
     }
     __syncwarp();
     if (lane == 0) {

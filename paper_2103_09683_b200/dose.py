@@ -135,6 +135,11 @@ _SIGS = {
     "dg_partition_lengths": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p]),
     "dg_kernel_times": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.POINTER(C.c_uint32)]),
     "dg_seeded_vector": (None, [C.c_uint64, C.c_uint64, C.c_void_p]),
+    "dg_set_gather_targets": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.c_uint32]),
+    "dg_ipc_alloc": (C.c_int, [C.c_uint64, C.c_int32, C.POINTER(C.c_void_p), C.c_void_p]),
+    "dg_ipc_open": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]),
+    "dg_ipc_close": (C.c_int, [C.c_void_p]),
+    "dg_ipc_free": (C.c_int, [C.c_void_p]),
     "dg_strerror": (C.c_char_p, [C.c_int]),
     "dg_version": (C.c_char_p, []),
 }
@@ -303,6 +308,12 @@ class DoseEngine:
         _check(_lib().dg_dose(self._h, C.c_void_p(x_ptr), x_len, C.c_void_p(y_ptr), 0,
                               C.c_void_p(stream) if stream else None), "dg_dose")
 
+    def set_gather_targets(self, ptrs: Sequence[int]) -> None:
+        """Fused d gather: every later dose also writes its rows, at their global row index, into
+        each of these full-d device buffers (this rank's own and its peers' IPC mappings)."""
+        arr = (C.c_void_p * max(len(ptrs), 1))(*[C.c_void_p(p) for p in ptrs])
+        _check(_lib().dg_set_gather_targets(self._h, arr, len(ptrs)), "dg_set_gather_targets")
+
     def kernel_times(self) -> list:
         """Per-launch CUDA-event times + algorithmic bytes of the last profiled dose."""
         buf = (_KernelTime * 16)()
@@ -354,6 +365,55 @@ class DoseEngine:
 
     def __exit__(self, *a):
         self.close()
+
+
+class PeerBuffer:
+    """A device buffer of float64 that other processes can map (CUDA IPC, dg_ipc_*).
+
+    ``PeerBuffer(n, device)`` allocates and exports (``handle``: 64 bytes to send to the peers);
+    ``PeerBuffer.open(handle, n, device)`` maps a peer's buffer.  ``tensor()`` views it as a torch
+    tensor through ``__cuda_array_interface__`` (no copy)."""
+
+    def __init__(self, n: int, device: int = 0, *, _ptr: int = 0, _owner: bool = True,
+                 _handle: bytes = b""):
+        self.n, self.device, self.owner = int(n), int(device), _owner
+        if _ptr:
+            self.ptr, self.handle = _ptr, _handle
+            return
+        p = C.c_void_p()
+        hbuf = C.create_string_buffer(64)
+        _check(_lib().dg_ipc_alloc(self.n * 8, self.device, C.byref(p), hbuf), "dg_ipc_alloc")
+        self.ptr, self.handle = int(p.value), hbuf.raw
+
+    @classmethod
+    def open(cls, handle: bytes, n: int, device: int = 0) -> "PeerBuffer":
+        p = C.c_void_p()
+        hbuf = C.create_string_buffer(bytes(handle), 64)
+        _check(_lib().dg_ipc_open(hbuf, int(device), C.byref(p)), "dg_ipc_open")
+        return cls(n, device, _ptr=int(p.value), _owner=False, _handle=bytes(handle))
+
+    @property
+    def __cuda_array_interface__(self):
+        return {"shape": (self.n,), "typestr": "<f8", "data": (self.ptr, False), "version": 2,
+                "strides": None}
+
+    def tensor(self):
+        import torch
+        return torch.as_tensor(self, device=f"cuda:{self.device}")
+
+    def close(self) -> None:
+        if self.ptr:
+            if self.owner:
+                _lib().dg_ipc_free(C.c_void_p(self.ptr))
+            else:
+                _lib().dg_ipc_close(C.c_void_p(self.ptr))
+            self.ptr = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class ScatterEngine:

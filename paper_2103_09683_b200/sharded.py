@@ -92,6 +92,78 @@ class ShardedDose:
             return gather_dose(y_local, self.bounds, group)
         return None
 
+    def enable_fused_gather(self, group=None) -> "FusedGather":
+        """Switch this shard to the fused gather (see FusedGather); returns it."""
+        if self.engine is None:
+            raise ValueError("the fused gather needs the shard's DoseEngine")
+        self.fused = FusedGather(self.engine, self.bounds, self.device, group)
+        return self.fused
+
     def close(self):
+        if getattr(self, "fused", None) is not None:
+            self.fused.close()
+            self.fused = None
         if self.engine is not None:
             self.engine.close()
+
+
+class FusedGather:
+    """The d all-gather fused into the dose kernels over peer memory.
+
+    Every rank allocates a full-d buffer (``PeerBuffer``), the 64-byte CUDA IPC handles are
+    exchanged with ``all_gather_object`` (host plumbing, once), each rank maps its peers' buffers
+    and registers all ``world`` buffers with ``dg_set_gather_targets``.  A dose then stores each
+    finished row of this rank's shard into every rank's full d straight from the kernel epilogue
+    (NVLink / NVSwitch P2P stores), so the exchange overlaps the SpMV instead of following it as
+    a separate NCCL all-gather.  After ``dose`` returns on every rank (stream synchronised, then
+    a barrier), ``full`` holds the complete d on this rank.
+    """
+
+    def __init__(self, engine: DoseEngine, bounds, device: int, group=None):
+        import torch.distributed as dist
+
+        from .dose import PeerBuffer
+
+        self.engine, self.group, self.device = engine, group, device
+        n = int(bounds[-1])
+        self.mine = PeerBuffer(n, device)
+        handles = [None] * dist.get_world_size(group)
+        dist.all_gather_object(handles, self.mine.handle, group=group)
+        me = dist.get_rank(group)
+        self.peers = [None if g == me else PeerBuffer.open(h, n, device)
+                      for g, h in enumerate(handles)]
+        ptrs = [self.mine.ptr if g == me else self.peers[g].ptr for g in range(len(handles))]
+        engine.set_gather_targets(ptrs)
+        self.full = self.mine.tensor()
+
+    def dose(self, x, y_local, *, stream: int = 0):
+        """This rank's slice into y_local and into every rank's full d; returns this rank's full
+        d once every rank has finished (stream sync + barrier)."""
+        import torch
+        import torch.distributed as dist
+
+        self.engine.dose_device(x.data_ptr(), x.numel(), y_local.data_ptr(), stream=stream,
+                                sync=False)
+        if stream:
+            torch.cuda.ExternalStream(stream).synchronize()
+        else:
+            torch.cuda.synchronize()
+        dist.barrier(group=self.group)
+        return self.full
+
+    def close(self):
+        import torch.distributed as dist
+
+        if self.engine is not None and self.engine._h:
+            self.engine.set_gather_targets([])
+        # peers must stop writing into our buffer before it is freed
+        if dist.is_initialized():
+            dist.barrier(group=self.group)
+        for p in self.peers:
+            if p is not None:
+                p.close()
+        self.peers = []
+        if dist.is_initialized():
+            dist.barrier(group=self.group)
+        self.full = None
+        self.mine.close()
