@@ -210,6 +210,12 @@ typedef struct {
 } dg_kernel_time;
 int dg_kernel_times(const dg_handle* h, dg_kernel_time* out, uint32_t cap, uint32_t* n_out);
 
+/* Diagnostics (no reference counterpart): with DG_TRACE set at dg_create, the first tile wave
+ * of every dose records a timeline -- per CTA {start ns, end ns, window-wait cycles, warp-cycles}
+ * (4 * sm_count words), then per tile {claim ns, finish ns, CTA | segments << 16 | global-x << 62}.
+ * Copies up to cap words of the last dose's timeline; *n_out = 0 when tracing is off. */
+int dg_debug_trace(const dg_handle* h, uint64_t* out, uint64_t cap, uint64_t* n_out);
+
 /* ddm::seeded_vector (src/bench.cpp:31-36): x[k] = xoshiro256**(seed).next_double53(). */
 void dg_seeded_vector(uint64_t n, uint64_t seed, double* out);
 

@@ -200,13 +200,19 @@ int launch_tiles_cfg(Handle* h, const M& mat, const Acc* x, double* y, cudaStrea
   static const char* const kWaveName[] = {"tiles[w0]", "tiles[w1]", "tiles[w2]", "tiles[w3]",
                                           "tiles[w4]", "tiles[w5]", "tiles[w6]", "tiles[w7]",
                                           "tiles[w8+]"};
+  TileTrace tr{nullptr, nullptr};
+  if (h->d_trace) {  // diagnostic timeline of wave 0 (DG_TRACE)
+    const uint64_t n = 4ull * h->sm_count + 3ull * h->wave_tiles[0];
+    DG_CUDA(cudaMemsetAsync(h->d_trace, 0, n * sizeof(unsigned long long), s));
+    tr = {h->d_trace, h->d_trace + 4ull * h->sm_count};
+  }
   for (uint32_t w = 0; w < h->n_waves; ++w) {
     if (!h->wave_tiles[w]) continue;
     const int grid = std::min<int>(h->sm_count, static_cast<int>(h->wave_tiles[w]));
     k_tiles<M, Acc, kWarps, kU, kR, kP, kNB><<<grid, kWarps * 32, smem, s>>>(
         mat, x, static_cast<const Tile*>(h->d_tiles[w]), h->wave_tiles[w],
         static_cast<const Segment*>(h->d_segs[w]), static_cast<Acc*>(h->d_state), y,
-        h->d_counters + w, h->window_cols, sig, h->gt);
+        h->d_counters + w, h->window_cols, sig, h->gt, w == 0 ? tr : TileTrace{nullptr, nullptr});
     h->post(s, kWaveName[std::min<uint32_t>(w, 8)], h->wave_rows[w], h->wave_nnz[w]);
   }
   DG_CUDA(cudaGetLastError());
@@ -350,11 +356,18 @@ int finish_create(Handle* h, const std::vector<uint64_t>& lens) {
                                                                   h->nnz / (8ull * h->sm_count)));
   if (const char* tn = std::getenv("DG_TILE_NNZ")) h->tile_nnz = std::strtoull(tn, nullptr, 10);
   if (const char* tc = std::getenv("DG_TILE_CFG")) h->tile_cfg = std::atoi(tc);
+  if (const char* tg = std::getenv("DG_TILE_GUIDE")) h->tile_guide = std::strtoull(tg, nullptr, 10);
+  if (const char* tg = std::getenv("DG_TILE_GUIDE_MIN"))
+    h->tile_guide_min = std::strtoull(tg, nullptr, 10);
   if (const char* gm = std::getenv("DG_GLOBAL_MIN_LEN"))
     h->global_min_len = std::strtoull(gm, nullptr, 10);
   h->window_cols = window_bytes_for(h->tile_cfg, h->packed) / h->acc_bytes;
   DG_TRY(build_plan(h, lens));
   if (h->use_tiles) DG_TRY(plan_tiles(h, lens));
+  if (std::getenv("DG_TRACE") && h->use_tiles && h->wave_tiles[0]) {
+    h->trace_len = 4ull * h->sm_count + 3ull * h->wave_tiles[0];
+    DG_CUDA(cudaMalloc(&h->d_trace, h->trace_len * sizeof(unsigned long long)));
+  }
   // x staging is padded to a 16-byte multiple: the 1-D TMA moves 16-byte granules
   DG_CUDA(cudaMalloc(&h->d_x, (std::max<uint64_t>(h->cols, 1) + 4) * sizeof(double)));
   DG_CUDA(cudaMemset(h->d_x, 0, (std::max<uint64_t>(h->cols, 1) + 4) * sizeof(double)));
@@ -522,6 +535,7 @@ int dg_destroy(dg_handle* hh) {
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   cudaFree(h->d_row_ptr);
+  cudaFree(h->d_trace);
   cudaFree(h->d_col);
   cudaFree(h->d_val);
   cudaFree(h->d_packed);
@@ -662,6 +676,18 @@ int dg_kernel_times(const dg_handle* hh, dg_kernel_time* out, uint32_t cap, uint
                           : 12ull * h->cols;
     *n_out = i + 1;
   }
+  return DG_OK;
+}
+
+int dg_debug_trace(const dg_handle* hh, uint64_t* out, uint64_t cap, uint64_t* n_out) {
+  const Handle* h = reinterpret_cast<const Handle*>(hh);
+  if (!h || !n_out) return DG_ERR_INVALID_CONFIG;
+  *n_out = 0;
+  if (!h->d_trace) return DG_OK;
+  DG_CUDA(cudaSetDevice(h->device));
+  const uint64_t n = std::min<uint64_t>(cap, h->trace_len);
+  if (n) DG_CUDA(cudaMemcpy(out, h->d_trace, n * 8, cudaMemcpyDeviceToHost));
+  *n_out = n;
   return DG_OK;
 }
 

@@ -47,6 +47,8 @@ struct Handle {
   uint32_t acc_bytes = 8;          // shared-memory x element: 8 exact, 4 fp32
   uint32_t window_cols = 0;        // x window capacity per buffer (columns)
   uint64_t tile_nnz = 1024 * 1024;  // target nonzeros per tile (C2 sweep: 256K 3.06 ms, 1M 2.86)
+  uint64_t tile_guide = 2;             // guided tail: tiles <= remaining / (guide * SMs) (0: off)
+  uint64_t tile_guide_min = 64 * 1024;  // smallest guided tile (nonzeros)
   uint32_t n_waves = 0;
   uint64_t n_split_rows = 0, n_global_rows = 0;
   uint64_t short_max = 32;  // rows with len <= short_max use the sub-warp bins, others the tiles
@@ -57,6 +59,8 @@ struct Handle {
   void* d_segs[kMaxWaves] = {};
   void* d_state = nullptr;
   uint32_t* d_counters = nullptr;
+  unsigned long long* d_trace = nullptr;  // DG_TRACE diagnostic timeline (dg_debug_trace)
+  uint64_t trace_len = 0;
   int sm_count = 148;
   bool use_tiles = false;
   bool tiles_attr = false;

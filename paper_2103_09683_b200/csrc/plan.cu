@@ -200,6 +200,16 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
       for (const HostSeg& s : global_x) wnnz += s.n;
     const uint64_t tile_nnz = std::max<uint64_t>(
         4096, std::min<uint64_t>(h->tile_nnz, wnnz / (8ull * h->sm_count)));
+    // guided sizing: tiles are claimed in list order, so the kernel's tail is the duration of
+    // the last tiles claimed.  Once the work left in the wave drops below ~kGuide tiles per SM,
+    // tiles shrink with it (remaining / (kGuide * SMs)), down to guide_min nonzeros.
+    const uint64_t guide = h->tile_guide;
+    const uint64_t guide_min = std::min<uint64_t>(tile_nnz, h->tile_guide_min);
+    auto cap_nnz = [&]() -> uint64_t {
+      if (!guide) return tile_nnz;
+      const uint64_t rem = wnnz - wave_nnz;
+      return std::max(guide_min, std::min(tile_nnz, rem / (guide * h->sm_count)));
+    };
     for (uint32_t k = 0; k < K; ++k) {
       // signalled only when one wave finishes every row (else the last wave owns the rows)
       const uint16_t blk = h->n_waves == 1 ? static_cast<uint16_t>(k) : kNoBlock;
@@ -211,7 +221,8 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
       while (g < G.size()) {
         uint64_t nnz = 0;
         const uint32_t s0 = static_cast<uint32_t>(segs.size());
-        while (g < G.size() && (nnz == 0 || nnz + G[g].n <= tile_nnz)) {
+        const uint64_t cap = cap_nnz();
+        while (g < G.size() && (nnz == 0 || nnz + G[g].n <= cap)) {
           const HostSeg& q = G[g++];
           segs.push_back({q.p0, q.n, q.row, 0, 0, q.flags});
           nnz += q.n;
@@ -231,9 +242,10 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
         uint32_t hi = S[i].chi;
         uint64_t nnz = 0;
         size_t j = i;
+        const uint64_t cap = cap_nnz();
         while (j < S.size()) {
           const uint32_t nhi = std::max(hi, S[j].chi);
-          if (j > i && (static_cast<uint64_t>(nhi) - xlo + 1 > W || nnz + S[j].n > tile_nnz)) break;
+          if (j > i && (static_cast<uint64_t>(nhi) - xlo + 1 > W || nnz + S[j].n > cap)) break;
           hi = nhi;
           nnz += S[j].n;
           ++j;

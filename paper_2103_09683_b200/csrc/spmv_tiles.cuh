@@ -55,6 +55,19 @@ struct BlockSignal {
   uint32_t epoch;
 };
 
+// Diagnostic timeline (DG_TRACE, dg_debug_trace): per CTA {start ns, end ns, cycles warps spent
+// waiting for a window buffer, warp-cycles alive}; per tile {claim ns, finish ns, CTA}.
+// cta == nullptr disables it (the default).
+struct TileTrace {
+  unsigned long long* cta;
+  unsigned long long* tile;
+};
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -374,7 +387,8 @@ template <class M, typename Acc, int WARPS, int U, int R = 0, int P = 0, int NB 
 __global__ void __launch_bounds__(WARPS * 32, 1)
     k_tiles(M mat, const Acc* __restrict__ x, const Tile* __restrict__ tiles, uint32_t n_tiles,
             const Segment* __restrict__ segs, Acc* __restrict__ state, double* __restrict__ y,
-            uint32_t* __restrict__ counter, uint32_t wcap, BlockSignal sig, GatherTargets gt) {
+            uint32_t* __restrict__ counter, uint32_t wcap, BlockSignal sig, GatherTargets gt,
+            TileTrace tr) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[NB];
   __shared__ uint32_t tile_of[NB], seg_next[NB], done[NB];
@@ -389,6 +403,11 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     done[b] = 0;
     if (t < n_tiles) {
       const Tile T = tiles[t];
+      if (tr.cta) {  // {claim ns, -, CTA | n_segments << 16 | global-x << 62}
+        tr.tile[3ull * t] = gtimer_ns();
+        tr.tile[3ull * t + 2] = blockIdx.x | (static_cast<unsigned long long>(T.seg1 - T.seg0) << 16) |
+                                (static_cast<unsigned long long>(T.xlen == 0) << 62);
+      }
       // order earlier generic-proxy reads of this buffer before the async-proxy overwrite
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       const uint32_t bytes = T.xlen * static_cast<uint32_t>(sizeof(Acc));  // 0: global-x tile
@@ -430,8 +449,17 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 
   uint32_t phases = 0;
   int b = 0;
+  const long long clk0 = clock64();
+  long long wait_cyc = 0;
+  if (tr.cta && threadIdx.x == 0) tr.cta[4ull * blockIdx.x] = gtimer_ns();
   for (;;) {
-    mbar_wait(&full[b], (phases >> b) & 1u);
+    if (tr.cta) {
+      const long long w0 = clock64();
+      mbar_wait(&full[b], (phases >> b) & 1u);
+      wait_cyc += clock64() - w0;
+    } else {
+      mbar_wait(&full[b], (phases >> b) & 1u);
+    }
     phases ^= 1u << b;
     const uint32_t t = *reinterpret_cast<volatile uint32_t*>(&tile_of[b]);
     if (t >= n_tiles) break;
@@ -459,6 +487,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       if (sig.left) __threadfence(); else __threadfence_block();
       if (atomicAdd(&done[b], 1u) == WARPS - 1) {  // the tile is finished
         __threadfence_block();
+        if (tr.cta) tr.tile[3ull * t + 1] = gtimer_ns();
         if (sig.left && T.blk != kNoBlock) {
           __threadfence();
           if (atomicSub(&sig.left[T.blk], 1u) == 1u) {
@@ -473,6 +502,11 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     }
     __syncwarp();
     b = b + 1 == NB ? 0 : b + 1;
+  }
+  if (tr.cta && lane == 0) {
+    atomicAdd(&tr.cta[4ull * blockIdx.x + 2], static_cast<unsigned long long>(wait_cyc));
+    atomicAdd(&tr.cta[4ull * blockIdx.x + 3], static_cast<unsigned long long>(clock64() - clk0));
+    atomicMax(&tr.cta[4ull * blockIdx.x + 1], gtimer_ns());
   }
 }
 

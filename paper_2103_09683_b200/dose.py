@@ -134,6 +134,7 @@ _SIGS = {
     "dg_partition_rows": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p]),
     "dg_partition_lengths": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p]),
     "dg_kernel_times": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.POINTER(C.c_uint32)]),
+    "dg_debug_trace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]),
     "dg_seeded_vector": (None, [C.c_uint64, C.c_uint64, C.c_void_p]),
     "dg_set_gather_targets": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.c_uint32]),
     "dg_ipc_alloc": (C.c_int, [C.c_uint64, C.c_int32, C.POINTER(C.c_void_p), C.c_void_p]),
@@ -321,6 +322,15 @@ class DoseEngine:
         _check(_lib().dg_kernel_times(self._h, buf, 16, C.byref(n)), "dg_kernel_times")
         return [{"name": buf[i].name.decode(), "ms": buf[i].ms, "bytes": buf[i].bytes,
                  "rows": buf[i].rows, "nnz": buf[i].nnz} for i in range(n.value)]
+
+    def debug_trace(self) -> np.ndarray:
+        """The DG_TRACE timeline of the last dose (uint64 words, see dg_debug_trace); empty when
+        the handle was created without DG_TRACE."""
+        cap = 4 * 1024 + 3 * 1_000_000
+        buf = np.zeros(cap, dtype=np.uint64)
+        n = C.c_uint64()
+        _check(_lib().dg_debug_trace(self._h, buf.ctypes.data, cap, C.byref(n)), "dg_debug_trace")
+        return buf[:n.value].copy()
 
     def last_timing(self) -> dict:
         t = _Timing()
