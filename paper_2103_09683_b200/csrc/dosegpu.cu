@@ -179,12 +179,13 @@ void launch_group(Handle* h, int b, const char* name, cudaStream_t s, const M& m
 
 // One persistent launch per wave (one CTA per SM): wave k continues the segments whose lane
 // partials wave k-1 stored.
-template <class M, typename Acc, int kWarps, int kU, int kR = 0, int kP = 0, int kNB = 2>
+template <class M, typename Acc, int kWarps, int kU, int kR = 0, int kP = 0, int kNB = 2,
+          bool kCarry = true>
 int launch_tiles_cfg(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t s) {
   const size_t smem = static_cast<size_t>(kNB) * h->window_cols * sizeof(Acc) +
                       ring_smem_bytes<kWarps, kR>();
   if (!h->tiles_attr) {  // a handle has one (M, Acc, config) and one device
-    DG_CUDA(cudaFuncSetAttribute(k_tiles<M, Acc, kWarps, kU, kR, kP, kNB>,
+    DG_CUDA(cudaFuncSetAttribute(k_tiles<M, Acc, kWarps, kU, kR, kP, kNB, kCarry>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
     h->tiles_attr = true;
@@ -206,14 +207,18 @@ int launch_tiles_cfg(Handle* h, const M& mat, const Acc* x, double* y, cudaStrea
     DG_CUDA(cudaMemsetAsync(h->d_trace, 0, n * sizeof(unsigned long long), s));
     tr = {h->d_trace, h->d_trace + 4ull * h->sm_count};
   }
+  const Carry<Acc> carry{static_cast<Acc*>(h->d_state)};
   for (uint32_t w = 0; w < h->n_waves; ++w) {
     if (!h->wave_tiles[w]) continue;
     const int grid = std::min<int>(h->sm_count, static_cast<int>(h->wave_tiles[w]));
-    k_tiles<M, Acc, kWarps, kU, kR, kP, kNB><<<grid, kWarps * 32, smem, s>>>(
+    k_tiles<M, Acc, kWarps, kU, kR, kP, kNB, kCarry><<<grid, kWarps * 32, smem, s>>>(
         mat, x, static_cast<const Tile*>(h->d_tiles[w]), h->wave_tiles[w],
-        static_cast<const Segment*>(h->d_segs[w]), static_cast<Acc*>(h->d_state), y,
-        h->d_counters + w, h->window_cols, sig, h->gt, w == 0 ? tr : TileTrace{nullptr, nullptr});
-    h->post(s, kWaveName[std::min<uint32_t>(w, 8)], h->wave_rows[w], h->wave_nnz[w]);
+        static_cast<const Segment*>(h->d_segs[w]), carry, y, h->d_counters + w, h->window_cols,
+        sig, h->gt, w == 0 ? tr : TileTrace{nullptr, nullptr});
+    if (h->fused_waves)
+      h->post(s, "tiles[fused]", h->fused_rows, h->fused_nnz);
+    else
+      h->post(s, kWaveName[std::min<uint32_t>(w, 8)], h->wave_rows[w], h->wave_nnz[w]);
   }
   DG_CUDA(cudaGetLastError());
   return DG_OK;
@@ -250,13 +255,25 @@ int launch_tiles(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t 
       case 11: return launch_tiles_cfg<M, Acc, 32, 8, 0, 0>(h, mat, x, y, s);
       case 12: return launch_tiles_cfg<M, Acc, 32, 8, 0, kP, 3>(h, mat, x, y, s);
       case 13: return launch_tiles_cfg<M, Acc, 32, 8, 0, kP, 4>(h, mat, x, y, s);
+      // (measured, rejected: cp.async.bulk.prefetch.L2 by one lane instead of per-line
+      //  prefetches, P = 2/4/8 -- C2 2.94-3.00 ms vs 2.80; profiles/README.md)
       default:
+        if (!h->n_carry_slots)  // no split rows: the carry code is compiled out
+          return launch_tiles_cfg<M, Acc, Handle::kTileWarps, Handle::kTileUnroll, 0, kP, 2, false>(
+              h, mat, x, y, s);
         return launch_tiles_cfg<M, Acc, Handle::kTileWarps, Handle::kTileUnroll, 0, kP>(h, mat, x,
                                                                                        y, s);
     }
   }
   // SoA elements take two registers each: 24 warps leave room for two U = 8 batches
-  return launch_tiles_cfg<M, Acc, 24, Handle::kTileUnroll, 0, kP>(h, mat, x, y, s);
+  if (!h->n_carry_slots)
+    return launch_tiles_cfg<M, Acc, 24, Handle::kTileUnroll, 0, kP, 2, false>(h, mat, x, y, s);
+  // split rows: 20 warps leave 96 registers, room for the carried-partials peek (C4: 6.70 ms
+  // vs 6.80 at 24 warps without the peek, 7.37 at 16 warps)
+  switch (h->tile_cfg) {
+    case 30: return launch_tiles_cfg<M, Acc, 24, Handle::kTileUnroll, 0, kP>(h, mat, x, y, s);
+    default: return launch_tiles_cfg<M, Acc, 20, Handle::kTileUnroll, 0, kP>(h, mat, x, y, s);
+  }
 }
 
 // Bytes of one x-window buffer: what is left of the 227 KB of shared memory per CTA after the
@@ -590,7 +607,7 @@ int dg_dose(dg_handle* hh, const double* x, uint64_t x_len, double* y, uint32_t 
   // Host d: download row block k as soon as the tile kernel publishes its completion, while it
   // still works on later blocks (one wave only: with carried partials the last wave owns rows).
   const char* no_ovl = std::getenv("DG_NO_OVERLAP");
-  const bool overlap = !y_dev && h->rows && h->use_tiles && h->n_waves == 1 &&
+  const bool overlap = !y_dev && h->rows && h->use_tiles && (h->n_waves == 1 || h->fused_waves) &&
                        h->n_blocks > 1 && dg::wait_value_fn() && !(no_ovl && *no_ovl == '1');
   h->signal_blocks = overlap;
   if (overlap) ++h->epoch;

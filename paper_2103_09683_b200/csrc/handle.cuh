@@ -41,7 +41,7 @@ struct Handle {
   uint64_t bin_nnz[kNumBins] = {};
   uint64_t plan_bytes = 0, nonempty_rows = 0;
   // ... and column-windowed tiles of row segments, per wave (plan.cu, spmv_tiles.cuh)
-  static constexpr uint32_t kMaxWaves = 32;
+  static constexpr uint32_t kMaxWaves = 64;
   static constexpr int kTileWarps = 32;
   static constexpr int kTileUnroll = 8;
   uint32_t acc_bytes = 8;          // shared-memory x element: 8 exact, 4 fp32
@@ -58,6 +58,9 @@ struct Handle {
   void* d_tiles[kMaxWaves] = {};
   void* d_segs[kMaxWaves] = {};
   void* d_state = nullptr;
+  bool fused_waves = false;            // all waves in one launch (wave 0's list)
+  uint64_t n_carry_slots = 0;          // split-row boundaries (32 partials each, Carry)
+  uint64_t fused_rows = 0, fused_nnz = 0;
   uint32_t* d_counters = nullptr;
   unsigned long long* d_trace = nullptr;  // DG_TRACE diagnostic timeline (dg_debug_trace)
   uint64_t trace_len = 0;
@@ -67,7 +70,8 @@ struct Handle {
   int tile_cfg = 0;  // DG_TILE_CFG: alternative (warps, U) configurations for A/B
 
   // output row blocks (plan.cu): the d download of block k overlaps the kernel's later blocks
-  static constexpr uint32_t kMaxBlocks = 8;
+  static constexpr uint32_t kMaxBlocks = 64;     // DG_BLOCKS range
+  static constexpr uint32_t kDefaultBlocks = 8;
   uint32_t n_blocks = 1;
   uint64_t blk_row0[kMaxBlocks + 1] = {};
   uint32_t blk_tiles[kMaxBlocks] = {};

@@ -3,11 +3,14 @@
 // Replaces the reference's scheduling (parallel_blocks: equal row-count blocks per std::thread,
 // src/spmv.cpp:17-32) with a device-oriented plan built once at dg_create:
 //   * rows with 1 <= len <= 32  -> bins by next_pow2(len), G lanes per row (k_group_*)
-//   * rows with len > 32        -> segments: a row whose column span fits a shared-memory window
-//                                  is one segment; a wider row is cut greedily into position
-//                                  ranges whose column spans fit (wave k = k-th segment of a row)
-//   * per wave, segments sorted by first column and cut into tiles (window <= W columns,
-//     ~kTileNnz nonzeros); inside a tile, longest segment first.
+//   * rows with len > 32        -> segments: a sparse row spanning <= W/3 columns, or a dense
+//                                  row spanning <= one shared-memory window (W columns), is one
+//                                  segment; a dense row wider than a window reads x from global
+//                                  memory; a wider sparse row is cut greedily into position ranges
+//                                  spanning <= W/3 columns (wave k = k-th segment of a row)
+//   * per wave, narrow segments binned into a fixed grid of windows, wide ones packed greedily
+//     by first column; tiles of <= W columns and ~tile_nnz nonzeros (guided: smaller at the
+//     end); inside a tile, longest segment first.  Waves run in one launch (fused) by default.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -33,7 +36,8 @@ __global__ void k_row_extents(M mat, const uint64_t* __restrict__ rp, uint64_t r
   }
 }
 
-// Greedy cut of wide rows: a segment starting at column c ends before the first column >= c+Ws.
+// Greedy cut of wide sparse rows: a segment starting at column c ends before the first column
+// >= c + ws (ws = the narrow bound A of plan_tiles_typed).
 template <class M>
 __global__ void k_split_rows(M mat, const uint64_t* __restrict__ rp,
                              const uint32_t* __restrict__ rows, uint32_t n_rows,
@@ -76,6 +80,10 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
   const uint32_t align = 16u / h->acc_bytes;                  // elements per 16 B (TMA alignment)
   const uint32_t W = h->window_cols;                          // window capacity (columns)
   const uint32_t ws = W - align;                              // max segment span
+  // narrow bound: sparse segments are kept within A columns so they pack into the fixed grid of
+  // windows below (stride W - A); dense rows may span a whole window (their lanes read
+  // consecutive x, so they share a window with few others anyway)
+  const uint32_t A = (W / 3) / align * align;
   std::vector<uint64_t> rp(rows + 1, 0);
   for (uint64_t r = 0; r < rows; ++r) rp[r + 1] = rp[r] + lens[r];
 
@@ -102,11 +110,12 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     const uint32_t c0 = ext[r].x, c1 = ext[r].y;
     const uint64_t span = static_cast<uint64_t>(c1) - c0 + 1;
     const uint16_t whole = static_cast<uint16_t>(kSegFirst | kSegLast);
-    const bool dense_long = lens[r] >= h->global_min_len && 4 * lens[r] >= 3 * span;
-    if (span <= ws && !dense_long) {
+    const bool dense = 4 * lens[r] >= 3 * span;
+    const bool dense_long = lens[r] >= h->global_min_len && dense;
+    if ((span <= A || (dense && span <= ws)) && !dense_long) {
       waves[0].push_back({rp[r], static_cast<uint32_t>(lens[r]), static_cast<uint32_t>(r), 0, c0,
                           c1, 0, whole});
-    } else if (4 * lens[r] >= 3 * span) {
+    } else if (dense) {
       global_x.push_back({rp[r], static_cast<uint32_t>(lens[r]), static_cast<uint32_t>(r), 0, c0,
                           c1, 0, static_cast<uint16_t>(whole | kSegGlobalX)});
     } else {
@@ -118,7 +127,7 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     std::vector<uint64_t> off(wide.size() + 1, 0);
     for (size_t i = 0; i < wide.size(); ++i) {
       const uint64_t span = static_cast<uint64_t>(ext[wide[i]].y) - ext[wide[i]].x + 1;
-      off[i + 1] = off[i] + span / (ws / 2 + 1) + 2;  // each segment but the last covers >= ws cols
+      off[i + 1] = off[i] + span / A + 2;  // every segment but the last advances >= A columns
     }
     const uint64_t total = off.back();
     uint32_t *d_rows = nullptr, *d_cnt = nullptr;
@@ -139,7 +148,7 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
       cu(cudaMemcpy(d_off, off.data(), (wide.size() + 1) * 8, cudaMemcpyHostToDevice));
       k_split_rows<M><<<grid_for(wide.size(), 128), 128>>>(
           mat, h->d_row_ptr, d_rows, static_cast<uint32_t>(wide.size()),
-          d_off, ws, d_pos, d_cext, d_cnt);
+          d_off, A, d_pos, d_cext, d_cnt);
       cu(cudaGetLastError());
       cu(cudaMemcpy(pos.data(), d_pos, total * 8, cudaMemcpyDeviceToHost));
       cu(cudaMemcpy(cext.data(), d_cext, total * sizeof(uint2), cudaMemcpyDeviceToHost));
@@ -147,19 +156,25 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     }
     cudaFree(d_rows); cudaFree(d_cnt); cudaFree(d_off); cudaFree(d_pos); cudaFree(d_cext);
     if (st) return st;
+    // carry slots: segment k of a split row writes slot base + k, segment k + 1 reads it
+    uint64_t base = 0;
     for (size_t i = 0; i < wide.size(); ++i) {
       const uint32_t r = wide[i];
       const uint64_t end = rp[r + 1];
+      if (base + cnt[i] > 0xFFFFFFFFull) return DG_ERR_UNSUPPORTED_FEATURE;
       for (uint32_t k = 0; k < cnt[i]; ++k) {
         const uint64_t p = pos[off[i] + k];
         const uint64_t q = k + 1 < cnt[i] ? pos[off[i] + k + 1] : end;
         if (waves.size() <= k) waves.resize(k + 1);
-        uint16_t flags = (k == 0 ? kSegFirst : 0) | (k + 1 == cnt[i] ? kSegLast : 0);
-        waves[k].push_back({p, static_cast<uint32_t>(q - p), r, static_cast<uint32_t>(i),
+        uint16_t flags = (k == 0 ? kSegFirst : 0) | (k + 1 == cnt[i] ? kSegLast : 0) |
+                         static_cast<uint16_t>(k << kSegWaveShift);
+        waves[k].push_back({p, static_cast<uint32_t>(q - p), r, static_cast<uint32_t>(base + k),
                             cext[off[i] + k].x, cext[off[i] + k].y,
                             static_cast<uint16_t>((p - rp[r]) & 31u), flags});
       }
+      base += cnt[i] - 1;
     }
+    h->n_carry_slots = base;
   }
 
   // 3. tiles per wave
@@ -169,7 +184,7 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
   h->n_global_rows = global_x.size();
   // Output row blocks: contiguous, byte-balanced row ranges whose tiles are listed block after
   // block, so block k of d is complete (and can be downloaded) while later blocks still run.
-  uint32_t K = h->nnz >= (16ull << 20) ? Handle::kMaxBlocks : 1;
+  uint32_t K = h->nnz >= (16ull << 20) ? Handle::kDefaultBlocks : 1;
   if (const char* kb = std::getenv("DG_BLOCKS"))
     K = std::max<uint32_t>(1, std::min<uint32_t>(Handle::kMaxBlocks, std::atoi(kb)));
   {
@@ -184,6 +199,19 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     return static_cast<uint32_t>(std::upper_bound(h->blk_row0, h->blk_row0 + K + 1, row) -
                                  h->blk_row0) - 1;
   };
+  // Several waves: one launch for all of them by default (fused: tiles listed wave after wave,
+  // segment k of a row waits on the row's flag, Carry in spmv_tiles.cuh) -- one kernel tail
+  // instead of one per wave.  DG_FUSE_WAVES=0 keeps one launch per wave.
+  h->fused_waves = h->n_waves > 1;
+  if (const char* fw = std::getenv("DG_FUSE_WAVES")) h->fused_waves = h->fused_waves && std::atoi(fw);
+  std::vector<uint64_t> later_nnz(h->n_waves + 1, 0);  // nonzeros of the waves after w
+  for (uint32_t w = h->n_waves; w-- > 0;) {
+    later_nnz[w] = later_nnz[w + 1];
+    for (const HostSeg& q : waves[w]) later_nnz[w] += q.n;
+  }
+  std::vector<Tile> all_tiles;
+  std::vector<Segment> all_segs;
+  uint64_t all_rows = 0;
   for (uint32_t w = 0; w < h->n_waves; ++w) {
     std::vector<std::vector<HostSeg>> win(K), glob(K);
     for (const HostSeg& s : waves[w]) win[blk_of(s.row)].push_back(s);
@@ -198,8 +226,14 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     for (const HostSeg& s : waves[w]) wnnz += s.n;
     if (w == 0)
       for (const HostSeg& s : global_x) wnnz += s.n;
+    // (fused waves: one launch, so the rule applies to all waves together)
+    uint64_t size_nnz = wnnz;
+    if (h->fused_waves) {
+      size_nnz = later_nnz[0];
+      for (const HostSeg& q : global_x) size_nnz += q.n;
+    }
     const uint64_t tile_nnz = std::max<uint64_t>(
-        4096, std::min<uint64_t>(h->tile_nnz, wnnz / (8ull * h->sm_count)));
+        4096, std::min<uint64_t>(h->tile_nnz, size_nnz / (8ull * h->sm_count)));
     // guided sizing: tiles are claimed in list order, so the kernel's tail is the duration of
     // the last tiles claimed.  Once the work left in the wave drops below ~kGuide tiles per SM,
     // tiles shrink with it (remaining / (kGuide * SMs)), down to guide_min nonzeros.
@@ -207,12 +241,14 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     const uint64_t guide_min = std::min<uint64_t>(tile_nnz, h->tile_guide_min);
     auto cap_nnz = [&]() -> uint64_t {
       if (!guide) return tile_nnz;
-      const uint64_t rem = wnnz - wave_nnz;
+      const uint64_t rem = wnnz - wave_nnz + (h->fused_waves ? later_nnz[w + 1] : 0);
       return std::max(guide_min, std::min(tile_nnz, rem / (guide * h->sm_count)));
     };
     for (uint32_t k = 0; k < K; ++k) {
-      // signalled only when one wave finishes every row (else the last wave owns the rows)
-      const uint16_t blk = h->n_waves == 1 ? static_cast<uint16_t>(k) : kNoBlock;
+      // signalled when one launch finishes every row: a single wave, or fused waves (the block
+      // completes with the last of its tiles in any wave)
+      const uint16_t blk =
+          h->n_waves == 1 || h->fused_waves ? static_cast<uint16_t>(k) : kNoBlock;
       const size_t tiles_before = tiles.size();
       // global-x tiles first (no window), longest rows first: the longest work items
       auto& G = glob[k];
@@ -231,25 +267,29 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
         }
         tiles.push_back({0, 0, blk, s0, static_cast<uint32_t>(segs.size())});
       }
-      // windowed tiles: segments by first column, cut at the window width or ~tile_nnz
+      // windowed tiles.  Narrow segments (span <= A = W/3) are binned into a fixed grid of
+      // windows [g*St, g*St + W), stride St = W - A: a segment whose first column lies in
+      // [g*St, (g+1)*St) fits window g, so the rare wide segments (e.g. a row's clusters in two
+      // adjacent beams, merged into one segment) cannot cut the tiles of narrow ones short.  Wide
+      // segments are packed greedily in first-column order.  Each bin: first-column order, cut
+      // at ~cap nonzeros.
       auto& S = win[k];
-      std::stable_sort(S.begin(), S.end(), [](const HostSeg& a, const HostSeg& b) {
+      const uint32_t St = W - A;
+      auto narrow = [&](const HostSeg& q) { return q.chi - q.clo + 1 <= A; };
+      std::stable_sort(S.begin(), S.end(), [&](const HostSeg& a, const HostSeg& b) {
+        const bool na = narrow(a), nb = narrow(b);
+        if (na != nb) return na;
+        const uint32_t ga = na ? a.clo / St : 0, gb = nb ? b.clo / St : 0;
+        if (ga != gb) return ga < gb;
         return a.clo != b.clo ? a.clo < b.clo : a.row < b.row;
       });
-      size_t i = 0;
-      while (i < S.size()) {
-        const uint32_t xlo = S[i].clo / align * align;
-        uint32_t hi = S[i].chi;
-        uint64_t nnz = 0;
-        size_t j = i;
-        const uint64_t cap = cap_nnz();
-        while (j < S.size()) {
-          const uint32_t nhi = std::max(hi, S[j].chi);
-          if (j > i && (static_cast<uint64_t>(nhi) - xlo + 1 > W || nnz + S[j].n > cap)) break;
-          hi = nhi;
-          nnz += S[j].n;
-          ++j;
+      auto emit = [&](size_t i, size_t j) {
+        uint32_t lo = S[i].clo, hi = S[i].chi;
+        for (size_t q = i; q < j; ++q) {
+          lo = std::min(lo, S[q].clo);
+          hi = std::max(hi, S[q].chi);
         }
+        const uint32_t xlo = lo / align * align;
         // longest segment first inside the tile (warps pull segments dynamically)
         std::stable_sort(S.begin() + i, S.begin() + j,
                          [](const HostSeg& a, const HostSeg& b) { return a.n > b.n; });
@@ -262,26 +302,77 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
           wave_nnz += S[q].n;
           wave_rows += (S[q].flags & kSegLast) ? 1 : 0;
         }
+      };
+      size_t i = 0;
+      while (i < S.size() && narrow(S[i])) {  // narrow: per grid window, cut by nonzeros
+        const uint32_t g = S[i].clo / St;
+        uint64_t nnz = 0;
+        size_t j = i;
+        const uint64_t cap = cap_nnz();
+        while (j < S.size() && narrow(S[j]) && S[j].clo / St == g && (j == i || nnz + S[j].n <= cap))
+          nnz += S[j++].n;
+        emit(i, j);
         i = j;
       }
-      if (w == 0) h->blk_tiles[k] = static_cast<uint32_t>(tiles.size() - tiles_before);
+      while (i < S.size()) {  // wide: greedy, cut at the window width or ~cap nonzeros
+        const uint32_t xlo = S[i].clo / align * align;
+        uint32_t hi = S[i].chi;
+        uint64_t nnz = 0;
+        size_t j = i;
+        const uint64_t cap = cap_nnz();
+        while (j < S.size()) {
+          const uint32_t nhi = std::max(hi, S[j].chi);
+          if (j > i && (static_cast<uint64_t>(nhi) - xlo + 1 > W || nnz + S[j].n > cap)) break;
+          hi = nhi;
+          nnz += S[j].n;
+          ++j;
+        }
+        emit(i, j);
+        i = j;
+      }
+      if (w == 0 || h->fused_waves)
+        h->blk_tiles[k] += static_cast<uint32_t>(tiles.size() - tiles_before);
     }
-    h->wave_tiles[w] = static_cast<uint32_t>(tiles.size());
     h->wave_nnz[w] = wave_nnz;
     h->wave_rows[w] = wave_rows;
+    if (h->fused_waves) {  // append to the single list: rebase the tiles' segment ranges
+      const uint32_t off = static_cast<uint32_t>(all_segs.size());
+      for (Tile& t : tiles) {
+        t.seg0 += off;
+        t.seg1 += off;
+      }
+      all_tiles.insert(all_tiles.end(), tiles.begin(), tiles.end());
+      all_segs.insert(all_segs.end(), segs.begin(), segs.end());
+      all_rows += wave_rows;
+      if (w + 1 < h->n_waves) continue;
+      tiles.swap(all_tiles);
+      segs.swap(all_segs);
+      for (uint32_t v = 1; v < h->n_waves; ++v) h->wave_tiles[v] = 0;
+      h->fused_rows = all_rows;
+      h->fused_nnz = 0;
+      for (uint32_t v = 0; v < h->n_waves; ++v) h->fused_nnz += h->wave_nnz[v];
+    }
+    const uint32_t lw = h->fused_waves ? 0 : w;  // the fused list is uploaded as launch 0
+    h->wave_tiles[lw] = static_cast<uint32_t>(tiles.size());
     if (!tiles.empty()) {
-      DG_CUDA(cudaMalloc(&h->d_tiles[w], tiles.size() * sizeof(Tile)));
-      DG_CUDA(cudaMemcpy(h->d_tiles[w], tiles.data(), tiles.size() * sizeof(Tile),
+      DG_CUDA(cudaMalloc(&h->d_tiles[lw], tiles.size() * sizeof(Tile)));
+      DG_CUDA(cudaMemcpy(h->d_tiles[lw], tiles.data(), tiles.size() * sizeof(Tile),
                          cudaMemcpyHostToDevice));
-      DG_CUDA(cudaMalloc(&h->d_segs[w], segs.size() * sizeof(Segment)));
-      DG_CUDA(cudaMemcpy(h->d_segs[w], segs.data(), segs.size() * sizeof(Segment),
+      DG_CUDA(cudaMalloc(&h->d_segs[lw], segs.size() * sizeof(Segment)));
+      DG_CUDA(cudaMemcpy(h->d_segs[lw], segs.data(), segs.size() * sizeof(Segment),
                          cudaMemcpyHostToDevice));
       h->plan_bytes += tiles.size() * sizeof(Tile) + segs.size() * sizeof(Segment);
     }
   }
-  if (h->n_split_rows) {
-    DG_CUDA(cudaMalloc(&h->d_state, h->n_split_rows * 32 * h->acc_bytes));
-    h->plan_bytes += h->n_split_rows * 32 * h->acc_bytes;
+  if (h->n_carry_slots) {
+    const uint64_t n = h->n_carry_slots * 32;
+    DG_CUDA(cudaMalloc(&h->d_state, n * h->acc_bytes));
+    h->plan_bytes += n * h->acc_bytes;
+    if (h->acc_bytes == 8)
+      k_carry_init<double><<<grid_for(n, 256), 256>>>(static_cast<double*>(h->d_state), n);
+    else
+      k_carry_init<float><<<grid_for(n, 256), 256>>>(static_cast<float*>(h->d_state), n);
+    DG_CUDA(cudaGetLastError());
   }
   DG_CUDA(cudaMalloc(&h->d_counters, Handle::kMaxWaves * sizeof(uint32_t)));
   DG_CUDA(cudaMalloc(&h->d_blk_left, Handle::kMaxBlocks * sizeof(uint32_t)));

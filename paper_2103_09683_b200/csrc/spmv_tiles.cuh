@@ -37,6 +37,78 @@ struct Segment {  // 24 bytes
   uint16_t flags;  // kSegFirst | kSegLast
 };
 constexpr uint16_t kSegFirst = 1, kSegLast = 2, kSegGlobalX = 4;
+constexpr uint32_t kSegWaveShift = 8;  // flags >> 8: the segment's index within its row (wave)
+
+// Lane partials carried between the segments (waves) of a split row.  Segment k of a row writes
+// its 32 lane partials to slot (row, k) -- Segment::slot -- and segment k + 1 reads them from
+// slot - 1.  Slots hold kCarryEmpty (a signalling NaN: arithmetic never produces one, every
+// partial is a quieted sum) until written, and the reader puts kCarryEmpty back for the next
+// dose, so a lane's partial is its own readiness flag: lane l of segment k + 1 spins only on its
+// own 8 bytes (one naturally aligned store / load: never torn), with no acquire/release pair
+// and no warp-wide flag.  That lets the warp `peek` the
+// next segment's carried partials when it grabs that segment (one segment ahead) and find them
+// already in registers at the switch.  The same code serves one launch per wave and all waves in
+// one launch (fused): in a persistent grid the wait is deadlock-free because tiles are claimed
+// wave after wave and a warp takes its segments in claim order, so a waiting segment only ever
+// waits on a lower wave's segment that is already claimed by a running warp.
+template <typename Acc>
+struct CarryBits;
+template <>
+struct CarryBits<double> {
+  static constexpr unsigned long long kEmpty = 0x7FF0000000000DC5ull;  // sNaN
+  __device__ static __forceinline__ bool empty(double v) {
+    return static_cast<unsigned long long>(__double_as_longlong(v)) == kEmpty;
+  }
+  __device__ static __forceinline__ double empty_value() {
+    return __longlong_as_double(static_cast<long long>(kEmpty));
+  }
+};
+template <>
+struct CarryBits<float> {
+  static constexpr unsigned kEmpty = 0x7F800DC5u;  // sNaN
+  __device__ static __forceinline__ bool empty(float v) { return __float_as_uint(v) == kEmpty; }
+  __device__ static __forceinline__ float empty_value() { return __uint_as_float(kEmpty); }
+};
+
+template <typename Acc>
+struct Carry {
+  using B = CarryBits<Acc>;
+  Acc* state;  // 32 partials per slot
+  __device__ __forceinline__ Acc* at(uint32_t slot, uint32_t lane) const {
+    return state + static_cast<uint64_t>(slot) * 32 + lane;
+  }
+  // start loading the partials segment (slot, flags) continues from (first segments: none).
+  // ld.global.cg: from L2, the coherence point (never a stale L1 line)
+  __device__ __forceinline__ Acc peek(uint32_t slot, uint32_t flags, uint32_t lane) const {
+    return (flags & kSegFirst) ? Acc(0) : __ldcg(at(slot - 1, lane));
+  }
+  // the partial to start from: the peeked value, re-read (ld.global.cv: fetched again every
+  // time) until the writer has stored it; the slot is emptied again for the next dose
+  __device__ __forceinline__ Acc take(uint32_t slot, uint32_t flags, uint32_t lane, Acc v) const {
+    if (flags & kSegFirst) return Acc(0);
+    Acc* p = at(slot - 1, lane);
+    while (B::empty(v)) {
+      __nanosleep(32);
+      v = __ldcv(p);
+    }
+    __stcg(p, B::empty_value());
+    return v;
+  }
+  __device__ __forceinline__ Acc in(uint32_t slot, uint32_t flags, uint32_t lane) const {
+    return take(slot, flags, lane, peek(slot, flags, lane));
+  }
+  __device__ __forceinline__ void out(uint32_t slot, uint32_t /*flags*/, uint32_t lane, Acc acc) const {
+    __stcg(at(slot, lane), acc);
+  }
+};
+
+// fill every carry slot with kCarryEmpty (at dg_create)
+template <typename Acc>
+__global__ void k_carry_init(Acc* __restrict__ state, uint64_t n) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    state[i] = CarryBits<Acc>::empty_value();
+}
 
 struct Tile {  // 16 bytes
   uint32_t xlo;   // x window start (16-byte aligned)
@@ -202,10 +274,14 @@ __device__ __forceinline__ void consume_batch(const typename M::Raw* r, uint32_t
 // Drain one tile's segment pool on one warp, software-pipelined across segment boundaries: the
 // next batch -- of the current segment, or batch 0 of the next segment -- is in flight while the
 // current batch is consumed; the next segment's descriptor is claimed one segment ahead.
-template <int U, int P, class M, typename Acc, class GrabFn>
+// CARRY = false: the plan has no split rows (every segment is a whole row), so the carry code
+// and its registers are compiled out.  PEEK: load the next segment's carried partials when it
+// is grabbed (2 more registers per lane; only where the register budget allows it -- spills in
+// this loop cost more than the load latency they hide).
+template <int U, int P, bool CARRY, bool PEEK, class M, typename Acc, class GrabFn>
 __device__ __forceinline__ void run_segments(const M& mat, const XWindow<Acc>& xw,
                                              const XGlobal<Acc>& xg, GrabFn&& grab,
-                                             Acc* __restrict__ state, double* __restrict__ y,
+                                             const Carry<Acc>& carry, double* __restrict__ y,
                                              const GatherTargets& gt, uint32_t lane) {
   using Ops = AccOps<Acc>;
   using Raw = typename M::Raw;
@@ -214,14 +290,12 @@ __device__ __forceinline__ void run_segments(const M& mat, const XWindow<Acc>& x
   SegRun cur = seg_run<U>(sd);
   Segment sn;
   bool have_next = grab(sn);
+  Acc carried_next = PEEK && have_next ? carry.peek(sn.slot, sn.flags, lane) : Acc(0);
   Raw ra[U], rb[U];
   const uint32_t safe = xw.xlo;
   uint32_t ma = load_batch<U>(mat, ra, cur, 0, lane, safe), mb = 0;
   prefetch_batches<U, P>(mat, cur, 1, lane);
-  auto init = [&](const SegRun& s) {
-    return (s.flags & kSegFirst) ? Acc(0) : state[static_cast<uint64_t>(s.slot) * 32 + lane];
-  };
-  Acc acc = init(cur);
+  Acc acc = CARRY ? carry.in(cur.slot, cur.flags, lane) : Acc(0);
   uint32_t bi = 0;
   // one pipeline step: consume (rc, mc), prefetch into (rn, mn); false when the pool is drained
   auto step = [&](const Raw* rc, uint32_t mc, Raw* rn, uint32_t& mn) -> bool {
@@ -239,7 +313,7 @@ __device__ __forceinline__ void run_segments(const M& mat, const XWindow<Acc>& x
       ++bi;
       return true;
     }
-    if (cur.flags & kSegLast) {
+    if (!CARRY || (cur.flags & kSegLast)) {
 #pragma unroll
       for (int off = 16; off >= 1; off /= 2) acc = Ops::add(acc, __shfl_down_sync(kFull, acc, off));
       if (lane == 0) {
@@ -247,13 +321,15 @@ __device__ __forceinline__ void run_segments(const M& mat, const XWindow<Acc>& x
         gt.store(cur.row, static_cast<double>(acc));
       }
     } else {
-      state[static_cast<uint64_t>(cur.slot) * 32 + lane] = acc;
+      if constexpr (CARRY) carry.out(cur.slot, cur.flags, lane, acc);
     }
     if (!have_next) return false;
     cur = seg_run<U>(sn);
     bi = 0;
-    acc = init(cur);
+    if constexpr (PEEK) acc = carry.take(cur.slot, cur.flags, lane, carried_next);
+    else acc = CARRY ? carry.in(cur.slot, cur.flags, lane) : Acc(0);
     have_next = grab(sn);
+    if (PEEK && have_next) carried_next = carry.peek(sn.slot, sn.flags, lane);
     return true;
   };
   for (;;) {
@@ -277,7 +353,7 @@ struct StageMeta {
 template <int U, int R, typename Acc, class GrabFn>
 __device__ __forceinline__ void run_segments_tma(const Packed16& mat, const XWindow<Acc>& xw,
                                                  const XGlobal<Acc>& xg, GrabFn&& grab,
-                                                 Acc* __restrict__ state, double* __restrict__ y,
+                                                 const Carry<Acc>& carry, double* __restrict__ y,
                                                  const GatherTargets& gt,
                                                  uint32_t lane, uint32_t* ring, StageMeta* meta,
                                                  uint64_t* bars, uint32_t& parity) {
@@ -342,7 +418,7 @@ __device__ __forceinline__ void run_segments_tma(const Packed16& mat, const XWin
     parity ^= 1u << cs;
     const StageMeta m = meta[cs];
     if (m.k == 0)
-      acc = (m.flags & kSegFirst) ? Acc(0) : state[static_cast<uint64_t>(m.slot) * 32 + lane];
+      acc = carry.in(m.slot, m.flags, lane);
     const uint32_t* st = ring + cs * kStageElems;
     uint32_t raw[U];
     uint32_t mask = 0;
@@ -365,7 +441,7 @@ __device__ __forceinline__ void run_segments_tma(const Packed16& mat, const XWin
           gt.store(m.row, static_cast<double>(acc));
         }
       } else {
-        state[static_cast<uint64_t>(m.slot) * 32 + lane] = acc;
+        carry.out(m.slot, m.flags, lane, acc);
       }
     }
     --inflight;
@@ -383,10 +459,11 @@ constexpr size_t ring_smem_bytes() {
 
 // Persistent: one CTA per SM; dynamic smem = 2 * wcap * sizeof(Acc) (two x-window buffers)
 // + ring_smem_bytes<WARPS, R>() (R > 0: TMA-streamed matrix, Packed16 only).
-template <class M, typename Acc, int WARPS, int U, int R = 0, int P = 0, int NB = 2>
+template <class M, typename Acc, int WARPS, int U, int R = 0, int P = 0, int NB = 2,
+          bool CARRY = true>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     k_tiles(M mat, const Acc* __restrict__ x, const Tile* __restrict__ tiles, uint32_t n_tiles,
-            const Segment* __restrict__ segs, Acc* __restrict__ state, double* __restrict__ y,
+            const Segment* __restrict__ segs, Carry<Acc> carry, double* __restrict__ y,
             uint32_t* __restrict__ counter, uint32_t wcap, BlockSignal sig, GatherTargets gt,
             TileTrace tr) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -476,10 +553,12 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       return true;
     };
     if constexpr (R > 0) {
-      run_segments_tma<U, R>(mat, xw, xg, grab, state, y, gt, lane, my_ring, my_meta, my_bars,
+      run_segments_tma<U, R>(mat, xw, xg, grab, carry, y, gt, lane, my_ring, my_meta, my_bars,
                              ring_parity);
     } else {
-      run_segments<U, P>(mat, xw, xg, grab, state, y, gt, lane);
+      // peek only with >= 96 registers per thread
+      constexpr bool kPeek = CARRY && WARPS * 32 * 96 <= 65536;
+      run_segments<U, P, CARRY, kPeek>(mat, xw, xg, grab, carry, y, gt, lane);
     }
     __syncwarp();
     if (lane == 0) {

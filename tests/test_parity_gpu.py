@@ -339,14 +339,26 @@ def test_generated_matrix_dose_matches_oracle(port):
     assert np.array_equal(bits(y), bits(port.spmv_rowchunk(m, x, 32, 4)))
 
 
-def test_multibeam_hstack_generator(port):
-    """C4 shape at small scale: 3 beams hstacked -> U32 indices, beam b's columns offset."""
+@pytest.mark.parametrize("fuse", ["1", "0"])
+def test_multibeam_hstack_generator(port, monkeypatch, fuse):
+    """C4 shape at small scale: 3 beams hstacked -> U32 indices, beam b's columns offset; rows
+    span several beams, so they are split into waves (fused into one launch, or not)."""
+    monkeypatch.setenv("DG_FUSE_WAVES", fuse)
     beams = [dg.Profile(20_000, 32_768, 0.0073, 0.70, 6.3386, 0.8278, 4096, 11 + b) for b in range(3)]
     with dg.DoseEngine.generate(beams) as e:
         assert e.info["cols"] == 3 * 32_768 and e.info["index_bytes"] == 4
         m = from_dg(e.copy_rows(0, 20_000))
         x = port.seeded_vector(m.cols, 1000)
         y = e.dose(x)
+        # the optimisation loop: x changes every evaluation, host and device d
+        import torch
+        yd = torch.empty(20_000, dtype=torch.float64, device="cuda")
+        for k in range(1, 4):
+            xk = port.seeded_vector(m.cols, 1000 + k)
+            want = bits(port.spmv_rowchunk(m, xk, 32, 4))
+            assert np.array_equal(bits(e.dose(xk)), want), k
+            e.dose_device(torch.from_numpy(xk).cuda().data_ptr(), m.cols, yd.data_ptr())
+            assert np.array_equal(yd.cpu().numpy().view(np.uint64), want), k
     assert port.validate(m) == 0
     assert np.array_equal(bits(y), bits(port.spmv_rowchunk(m, x, 32, 4)))
     with dg.DoseEngine.generate(beams[1]) as single:
@@ -408,15 +420,24 @@ def _wide_row_matrix(port, rows=3000, cols=40_000, seed=5):
     return Csr(rows, cols, HALF, U16, rp, col, vals)
 
 
+@pytest.mark.parametrize("fuse", ["1", "0"])
 @pytest.mark.parametrize("tile_nnz", ["4096", "262144"])
-def test_windowed_tiles_with_split_rows_bit_exact(port, monkeypatch, tile_nnz):
+def test_windowed_tiles_with_split_rows_bit_exact(port, monkeypatch, tile_nnz, fuse):
+    """Split rows carry lane partials between waves: in one launch (fused: per-row flags) or in
+    one launch per wave."""
     monkeypatch.setenv("DG_TILE_NNZ", tile_nnz)
+    monkeypatch.setenv("DG_FUSE_WAVES", fuse)
     m = _wide_row_matrix(port)
     x = port.seeded_vector(m.cols, 42)
     want = port.spmv_rowchunk(m, x, 32, 4)
     with dg.DoseEngine.from_csr(to_dg(m)) as e:
         got = e.dose(x)
-        assert e.info["n_kernels"] >= 2  # >= 2 waves (sparse wide rows are split)
+        if fuse == "0":
+            assert e.info["n_kernels"] >= 2  # >= 2 waves (sparse wide rows are split)
+        # repeated doses: the fused plan's per-row flags are epoch-tagged, never stale
+        for seed in (7, 8):
+            x2 = port.seeded_vector(m.cols, seed)
+            assert np.array_equal(bits(e.dose(x2)), bits(port.spmv_rowchunk(m, x2, 32, 4)))
     assert np.array_equal(bits(got), bits(want))
     for short_max in ("0", "32"):  # short rows folded into tiles / in sub-warp bins
         monkeypatch.setenv("DG_SHORT_MAX", short_max)
