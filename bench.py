@@ -37,7 +37,7 @@ FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c4", "c5"])
@@ -85,7 +85,10 @@ def measured_hbm_peak():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks + throttle reasons, sampled every 100 ms.  Started before the warm-up
+    (nvidia-smi's own start-up -- NVML init -- must not overlap the timed region); only the samples
+    taken inside [mark_start, mark_stop] are reported (all of them if the region was shorter than
+    one sampling period, with "in_region": false)."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
@@ -93,10 +96,11 @@ class ClockSampler:
     def __init__(self, device: int):
         self.rows = []
         self.proc = None
+        self.t0 = self.t1 = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200", "-i", str(device)], stdout=subprocess.PIPE,
+                 "-lms", "100", "-i", str(device)], stdout=subprocess.PIPE,
                 stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -107,23 +111,40 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) == 6:
-                self.rows.append(parts)
+                self.rows.append((time.time(), parts))
+
+    def wait_ready(self, timeout: float = 5.0):
+        """Block until nvidia-smi has produced its first sample (its start-up is over)."""
+        end = time.time() + timeout
+        while self.proc and not self.rows and time.time() < end:
+            time.sleep(0.02)
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_stop(self):
+        self.t1 = time.time()
 
     def stop(self):
         if self.proc:
-            time.sleep(0.25)
+            time.sleep(0.15)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
             except Exception:
                 self.proc.kill()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        rows = [r for t, r in self.rows
+                if self.t0 is not None and self.t1 is not None and self.t0 <= t <= self.t1 + 0.1]
+        in_region = bool(rows)
+        if not rows:
+            rows = [r for _, r in self.rows]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "samples": len(rows), "in_region": in_region}
 
 
 # ---------------------------------------------------------------------- CPU baselines ------
@@ -291,14 +312,17 @@ def run_ours(args):
         torch.cuda.synchronize()
         return a.elapsed_time(b)
 
+    clocks = ClockSampler(local)
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
+    clocks.wait_ready()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local)
+    clocks.mark_start()
     ms = timed(step, args.steps)
+    clocks.mark_stop()
     clk = clocks.stop()
     if dist:
         dist.barrier()

@@ -23,11 +23,14 @@ namespace dg {
 
 constexpr unsigned kFull = 0xffffffffu;
 
-// Exact binary16 -> double (ddm::decode_half, src/half.cpp:50-64): binary16 -> binary32 is exact
-// for every pattern (subnormals become normals, Inf/NaN stay), binary32 -> binary64 is exact.
-// SASS: HADD2.F32 + F2F.F64.F32.
+// Exact binary16 -> double (ddm::decode_half, src/half.cpp:50-64): cvt.f64.f16 is an exact
+// widening for every pattern (subnormals become normals, Inf/NaN stay).  SASS: one
+// F2F.F64.F16 reading the low half of the packed word directly (instead of HADD2.F32 +
+// F2F.F64.F32).
 __device__ __forceinline__ double widen(uint16_t h) {
-  return static_cast<double>(__half2float(__ushort_as_half(h)));
+  double d;
+  asm("{ .reg .f16 t; mov.b16 t, %1; cvt.f64.f16 %0, t; }" : "=d"(d) : "h"(h));
+  return d;
 }
 __device__ __forceinline__ double widen(float v) { return static_cast<double>(v); }
 __device__ __forceinline__ double widen(double v) { return v; }

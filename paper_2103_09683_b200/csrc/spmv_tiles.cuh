@@ -225,13 +225,17 @@ __device__ __forceinline__ uint32_t load_batch(const M& mat, typename M::Raw* r,
     for (int u = 0; u < U; ++u) r[u] = mat.load(base + 32 * u);
     return kFullMask<U>;
   }
-  uint32_t mask = 0;
+  // chunk u holds position rel = b0 + lane + 32u: valid for u in [ulo, uhi) with
+  // uhi = ceil((hi - b0 - lane) / 32) and ulo = ceil((lo - b0 - lane) / 32), clamped to [0, U]
+  const int t0 = static_cast<int>(b0 + lane);
+  const int th = static_cast<int>(s.hi) - t0, tl = static_cast<int>(s.lo) - t0;
+  const uint32_t uhi = th <= 0 ? 0u : min(static_cast<uint32_t>(U), static_cast<uint32_t>(th + 31) >> 5);
+  const uint32_t ulo = tl <= 0 ? 0u : min(static_cast<uint32_t>(U), static_cast<uint32_t>(tl + 31) >> 5);
+  const uint32_t mask = ((1u << uhi) - 1u) & ~((1u << ulo) - 1u);
 #pragma unroll
   for (int u = 0; u < U; ++u) {
-    const uint32_t rel = b0 + lane + 32 * u;
-    const bool ok = rel >= s.lo && rel < s.hi;
-    r[u] = ok ? mat.load(base + 32 * u) : M::filler(safe_col);
-    mask |= static_cast<uint32_t>(ok) << u;
+    r[u] = M::filler(safe_col);
+    if (mask & (1u << u)) r[u] = mat.load(base + 32 * u);
   }
   return mask;
 }
@@ -295,6 +299,7 @@ __device__ __forceinline__ void run_segments(const M& mat, const XWindow<Acc>& x
   const uint32_t safe = xw.xlo;
   uint32_t ma = load_batch<U>(mat, ra, cur, 0, lane, safe), mb = 0;
   prefetch_batches<U, P>(mat, cur, 1, lane);
+  bool sn_pf = false;  // the next segment's head (P + 1 batches) has been prefetched
   Acc acc = CARRY ? carry.in(cur.slot, cur.flags, lane) : Acc(0);
   uint32_t bi = 0;
   // one pipeline step: consume (rc, mc), prefetch into (rn, mn); false when the pool is drained
@@ -302,10 +307,15 @@ __device__ __forceinline__ void run_segments(const M& mat, const XWindow<Acc>& x
     const bool more = bi + 1 < cur.nbatch;
     if (more) mn = load_batch<U>(mat, rn, cur, bi + 1, lane, safe);
     else if (have_next) mn = load_batch<U>(mat, rn, seg_run<U>(sn), 0, lane, safe);
-    if constexpr (P > 0) {  // the L2 prefetch stream runs P batches ahead of the loads
+    if constexpr (P > 0) {  // the L2 prefetch stream runs P batches ahead of the loads; once
+      // it passes the end of this segment, the next segment's first P + 1 batches go at once
       const uint32_t pf = bi + 1 + P;
-      if (pf < cur.nbatch) prefetch_batches<U, 1>(mat, cur, pf, lane);
-      else if (have_next) prefetch_batches<U, 1>(mat, seg_run<U>(sn), pf - cur.nbatch, lane);
+      if (pf < cur.nbatch) {
+        prefetch_batches<U, 1>(mat, cur, pf, lane);
+      } else if (have_next && !sn_pf) {
+        sn_pf = true;
+        prefetch_batches<U, P + 1>(mat, seg_run<U>(sn), 0, lane);
+      }
     }
     if (cur.flags & kSegGlobalX) consume_batch<U, M>(rc, mc, xg, acc);
     else consume_batch<U, M>(rc, mc, xw, acc);
@@ -329,6 +339,7 @@ __device__ __forceinline__ void run_segments(const M& mat, const XWindow<Acc>& x
     if constexpr (PEEK) acc = carry.take(cur.slot, cur.flags, lane, carried_next);
     else acc = CARRY ? carry.in(cur.slot, cur.flags, lane) : Acc(0);
     have_next = grab(sn);
+    sn_pf = false;
     if (PEEK && have_next) carried_next = carry.peek(sn.slot, sn.flags, lane);
     return true;
   };

@@ -60,7 +60,8 @@ def ncu(tag, family):
                           capture_output=True, text=True).stdout
     hot = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "ncu_sass_hot.py"), rep,
                           "stall", "25"], capture_output=True, text=True).stdout
-    text = (f"# {tag}: ncu --set full --clock-control none, hot kernel k_tiles (C2, {family})\n"
+    cfg = "C4" if family == "c4" else "C2"
+    text = (f"# {tag}: ncu --set full --clock-control none, hot kernel k_tiles ({cfg}, {family})\n"
             + summ + "\n# hottest SASS by warp-stall samples (addr, executed, samples, instr)\n" + hot)
     open(os.path.join(PROF, f"{tag}_ncu_{family}.txt"), "w").write(text)
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
@@ -83,10 +84,12 @@ def main():
         launches(tag)
     tf = os.path.join(PROF, "dram_bytes_per_launch.json")
     traffic = json.load(open(tf)) if os.path.exists(tf) else {}
-    for fam in ("exact", "fp32"):
+    # keys: <config>:<accumulation>:<kernel name in dg_kernel_times> (read by bench.py)
+    for fam, key in (("exact", "c2:exact:tiles[w0]"), ("fp32", "c2:fp32:tiles[w0]"),
+                     ("c4", "c4:exact:tiles[fused]")):
         t = ncu(tag, fam)
         if t is not None:
-            traffic[f"c2:{fam}:[w0]"] = int(t)
+            traffic[key] = int(t)
             print(fam, "dram bytes per launch", t)
     json.dump(traffic, open(tf, "w"), indent=1, sort_keys=True)
 
