@@ -40,13 +40,21 @@ def launches(tag):
             per.setdefault(name, []).append(v)
     dose = {k: v for k, v in per.items() if "gen_" not in k and "cub::" not in k and
             "row_extents" not in k and "split_rows" not in k and "validate" not in k}
-    step = sum(sum(v) for v in dose.values()) / max(1, max(len(v) for v in dose.values()))
-    lines = [f"# {tag}: ncu launch list of `python bench.py --steps 3 --warmup 3` (C2), "
-             "gpu__time_duration.sum, --clock-control none (cold-cache, serialised launches)",
+
+    def family(k):  # the bench runs the exact family, then the fp32 side line
+        return "fp32" if ("float" in k or "f32" in k) else "exact"
+
+    # one dose of a family = the sum of its kernels' average launch times
+    step = collections.defaultdict(float)
+    for k, v in dose.items():
+        step[family(k)] += sum(v) / len(v)
+    lines = [f"# {tag}: ncu launch list of `python bench.py --steps 3 --warmup 3` (C2, exact "
+             "family then the fp32 side line), gpu__time_duration.sum, --clock-control none "
+             "(cold-cache, serialised launches); share = avg launch time / the family's dose",
              f"{'kernel':70s} {'launches':>8s} {'avg us':>10s} {'share of dose':>14s}"]
     for k, v in per.items():
         avg = sum(v) / len(v)
-        share = (sum(v) / len(v)) / step if k in dose else float("nan")
+        share = avg / step[family(k)] if k in dose else float("nan")
         lines.append(f"{k[:70]:70s} {len(v):8d} {avg:10.1f} {share:14.3f}")
     open(os.path.join(PROF, f"{tag}_launches.txt"), "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
