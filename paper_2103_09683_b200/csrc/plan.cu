@@ -177,16 +177,27 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     h->n_carry_slots = base;
   }
 
-  // 3. tiles per wave
+  // 3. tiles
   const uint64_t xcap = (h->cols + align - 1) / align * align;  // padded x length on device
   if (waves.size() > Handle::kMaxWaves) return DG_ERR_UNSUPPORTED_FEATURE;
   h->n_waves = static_cast<uint32_t>(waves.size());
   h->n_global_rows = global_x.size();
-  // Output row blocks: contiguous, byte-balanced row ranges whose tiles are listed block after
-  // block, so block k of d is complete (and can be downloaded) while later blocks still run.
+  // Several waves: one launch for all of them by default (fused: segment k + 1 of a row waits for
+  // segment k's carried partials, Carry in spmv_tiles.cuh) -- one kernel tail instead of one per
+  // wave.  DG_FUSE_WAVES=0 keeps one launch per wave.
+  h->fused_waves = h->n_waves > 1;
+  if (const char* fw = std::getenv("DG_FUSE_WAVES")) h->fused_waves = h->fused_waves && std::atoi(fw);
+  // Output row blocks: contiguous, byte-balanced row ranges.  A block's d is complete (and can be
+  // downloaded) once its tiles are done.  Fused waves list the (wave, block) groups diagonally --
+  // wave w of block b right after wave w - 1 of block b + lag -- with lag = K - 1 (wave after
+  // wave) by default.  Measured on C4: a short lag (64 blocks, lag 1 or 3, meant to read carried
+  // partials back while still in L2) makes segments wait on tiles still in flight -- ~296 tiles
+  // (2 per SM) of ~1M nonzeros are always in flight -- 7.95 / 6.83 ms vs 6.70 wave after wave.
   uint32_t K = h->nnz >= (16ull << 20) ? Handle::kDefaultBlocks : 1;
   if (const char* kb = std::getenv("DG_BLOCKS"))
     K = std::max<uint32_t>(1, std::min<uint32_t>(Handle::kMaxBlocks, std::atoi(kb)));
+  uint32_t lag = K - 1;
+  if (const char* lg = std::getenv("DG_WAVE_LAG")) lag = std::max(0, std::atoi(lg));
   {
     std::vector<uint64_t> b(K + 1);
     std::vector<uint32_t> l32(rows);
@@ -199,58 +210,63 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     return static_cast<uint32_t>(std::upper_bound(h->blk_row0, h->blk_row0 + K + 1, row) -
                                  h->blk_row0) - 1;
   };
-  // Several waves: one launch for all of them by default (fused: tiles listed wave after wave,
-  // segment k of a row waits on the row's flag, Carry in spmv_tiles.cuh) -- one kernel tail
-  // instead of one per wave.  DG_FUSE_WAVES=0 keeps one launch per wave.
-  h->fused_waves = h->n_waves > 1;
-  if (const char* fw = std::getenv("DG_FUSE_WAVES")) h->fused_waves = h->fused_waves && std::atoi(fw);
-  std::vector<uint64_t> later_nnz(h->n_waves + 1, 0);  // nonzeros of the waves after w
-  for (uint32_t w = h->n_waves; w-- > 0;) {
-    later_nnz[w] = later_nnz[w + 1];
-    for (const HostSeg& q : waves[w]) later_nnz[w] += q.n;
+  const uint32_t NW = h->n_waves;
+  std::vector<std::vector<std::vector<HostSeg>>> win(NW, std::vector<std::vector<HostSeg>>(K));
+  std::vector<std::vector<HostSeg>> glob(K);
+  for (uint32_t w = 0; w < NW; ++w)
+    for (const HostSeg& q : waves[w]) win[w][blk_of(q.row)].push_back(q);
+  for (const HostSeg& q : global_x) glob[blk_of(q.row)].push_back(q);
+  // emission order of the (wave, block) groups
+  std::vector<std::pair<uint32_t, uint32_t>> order;
+  if (h->fused_waves) {
+    for (uint32_t key = 0; key < K + (NW - 1) * (lag + 1); ++key)
+      for (uint32_t w = 0; w < NW; ++w)
+        if (key >= w * (lag + 1) && key - w * (lag + 1) < K) order.push_back({w, key - w * (lag + 1)});
+  } else {
+    for (uint32_t w = 0; w < NW; ++w)
+      for (uint32_t k = 0; k < K; ++k) order.push_back({w, k});
   }
-  std::vector<Tile> all_tiles;
-  std::vector<Segment> all_segs;
-  uint64_t all_rows = 0;
-  for (uint32_t w = 0; w < h->n_waves; ++w) {
-    std::vector<std::vector<HostSeg>> win(K), glob(K);
-    for (const HostSeg& s : waves[w]) win[blk_of(s.row)].push_back(s);
-    if (w == 0)
-      for (const HostSeg& s : global_x) glob[blk_of(s.row)].push_back(s);
-    std::vector<Tile> tiles;
-    std::vector<Segment> segs;
-    segs.reserve(waves[w].size() + (w == 0 ? global_x.size() : 0));
-    uint64_t wave_nnz = 0, wave_rows = 0;
-    // later waves are smaller: keep >= ~8 tiles per SM in every wave (no single-tile tails)
-    uint64_t wnnz = 0;
-    for (const HostSeg& s : waves[w]) wnnz += s.n;
-    if (w == 0)
-      for (const HostSeg& s : global_x) wnnz += s.n;
-    // (fused waves: one launch, so the rule applies to all waves together)
-    uint64_t size_nnz = wnnz;
-    if (h->fused_waves) {
-      size_nnz = later_nnz[0];
-      for (const HostSeg& q : global_x) size_nnz += q.n;
-    }
+  // one tile list per launch (fused: one launch)
+  const uint32_t NL = h->fused_waves ? 1 : NW;
+  std::vector<std::vector<Tile>> ltiles(NL);
+  std::vector<std::vector<Segment>> lsegs(NL);
+  std::vector<uint64_t> lnnz(NL, 0), ldone(NL, 0), lrows(NL, 0);
+  for (uint32_t w = 0; w < NW; ++w)
+    for (const HostSeg& q : waves[w]) lnnz[h->fused_waves ? 0 : w] += q.n;
+  for (const HostSeg& q : global_x) lnnz[0] += q.n;
+  std::vector<uint64_t> wnnz(NW, 0), wrows(NW, 0);
+  const uint32_t St = W - A;
+  auto narrow = [&](const HostSeg& q) { return q.chi - q.clo + 1 <= A; };
+  for (const auto& [w, k] : order) {
+    const uint32_t lw = h->fused_waves ? 0 : w;
+    std::vector<Tile>& tiles = ltiles[lw];
+    std::vector<Segment>& segs = lsegs[lw];
+    // ~8 tiles per SM at least in every launch (no single-tile tails), at most tile_nnz
     const uint64_t tile_nnz = std::max<uint64_t>(
-        4096, std::min<uint64_t>(h->tile_nnz, size_nnz / (8ull * h->sm_count)));
-    // guided sizing: tiles are claimed in list order, so the kernel's tail is the duration of
-    // the last tiles claimed.  Once the work left in the wave drops below ~kGuide tiles per SM,
-    // tiles shrink with it (remaining / (kGuide * SMs)), down to guide_min nonzeros.
+        4096, std::min<uint64_t>(h->tile_nnz, lnnz[lw] / (8ull * h->sm_count)));
+    // guided sizing: tiles are claimed in list order, so the kernel's tail is the duration of the
+    // last tiles claimed.  Once the work left in the launch drops below ~guide tiles per SM,
+    // tiles shrink with it (remaining / (guide * SMs)), down to guide_min nonzeros.
     const uint64_t guide = h->tile_guide;
     const uint64_t guide_min = std::min<uint64_t>(tile_nnz, h->tile_guide_min);
     auto cap_nnz = [&]() -> uint64_t {
       if (!guide) return tile_nnz;
-      const uint64_t rem = wnnz - wave_nnz + (h->fused_waves ? later_nnz[w + 1] : 0);
+      const uint64_t rem = lnnz[lw] - ldone[lw];
       return std::max(guide_min, std::min(tile_nnz, rem / (guide * h->sm_count)));
     };
-    for (uint32_t k = 0; k < K; ++k) {
-      // signalled when one launch finishes every row: a single wave, or fused waves (the block
-      // completes with the last of its tiles in any wave)
-      const uint16_t blk =
-          h->n_waves == 1 || h->fused_waves ? static_cast<uint16_t>(k) : kNoBlock;
-      const size_t tiles_before = tiles.size();
-      // global-x tiles first (no window), longest rows first: the longest work items
+    // signalled when one launch finishes every row: a single wave, or fused waves (a block
+    // completes with the last of its tiles in any wave)
+    const uint16_t blk = NW == 1 || h->fused_waves ? static_cast<uint16_t>(k) : kNoBlock;
+    const size_t tiles_before = tiles.size();
+    auto take = [&](const HostSeg& q) {
+      segs.push_back({q.p0, q.n, q.row, q.slot, q.lane0, q.flags});
+      ldone[lw] += q.n;
+      wnnz[w] += q.n;
+      const bool last = (q.flags & kSegLast) != 0;
+      wrows[w] += last;
+      lrows[lw] += last;
+    };
+    if (w == 0) {  // global-x tiles first (no window), longest rows first
       auto& G = glob[k];
       std::stable_sort(G.begin(), G.end(), [](const HostSeg& a, const HostSeg& b) { return a.n > b.n; });
       size_t g = 0;
@@ -259,110 +275,91 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
         const uint32_t s0 = static_cast<uint32_t>(segs.size());
         const uint64_t cap = cap_nnz();
         while (g < G.size() && (nnz == 0 || nnz + G[g].n <= cap)) {
-          const HostSeg& q = G[g++];
-          segs.push_back({q.p0, q.n, q.row, 0, 0, q.flags});
-          nnz += q.n;
-          wave_nnz += q.n;
-          ++wave_rows;
+          nnz += G[g].n;
+          take(G[g++]);
         }
         tiles.push_back({0, 0, blk, s0, static_cast<uint32_t>(segs.size())});
       }
-      // windowed tiles.  Narrow segments (span <= A = W/3) are binned into a fixed grid of
-      // windows [g*St, g*St + W), stride St = W - A: a segment whose first column lies in
-      // [g*St, (g+1)*St) fits window g, so the rare wide segments (e.g. a row's clusters in two
-      // adjacent beams, merged into one segment) cannot cut the tiles of narrow ones short.  Wide
-      // segments are packed greedily in first-column order.  Each bin: first-column order, cut
-      // at ~cap nonzeros.
-      auto& S = win[k];
-      const uint32_t St = W - A;
-      auto narrow = [&](const HostSeg& q) { return q.chi - q.clo + 1 <= A; };
-      std::stable_sort(S.begin(), S.end(), [&](const HostSeg& a, const HostSeg& b) {
-        const bool na = narrow(a), nb = narrow(b);
-        if (na != nb) return na;
-        const uint32_t ga = na ? a.clo / St : 0, gb = nb ? b.clo / St : 0;
-        if (ga != gb) return ga < gb;
-        return a.clo != b.clo ? a.clo < b.clo : a.row < b.row;
-      });
-      auto emit = [&](size_t i, size_t j) {
-        uint32_t lo = S[i].clo, hi = S[i].chi;
-        for (size_t q = i; q < j; ++q) {
-          lo = std::min(lo, S[q].clo);
-          hi = std::max(hi, S[q].chi);
-        }
-        const uint32_t xlo = lo / align * align;
-        // longest segment first inside the tile (warps pull segments dynamically)
-        std::stable_sort(S.begin() + i, S.begin() + j,
-                         [](const HostSeg& a, const HostSeg& b) { return a.n > b.n; });
-        uint32_t xlen = (hi - xlo + 1 + align - 1) / align * align;
-        if (xlo + xlen > xcap) xlen = static_cast<uint32_t>(xcap - xlo);
-        tiles.push_back({xlo, static_cast<uint16_t>(xlen), blk, static_cast<uint32_t>(segs.size()),
-                         static_cast<uint32_t>(segs.size() + (j - i))});
-        for (size_t q = i; q < j; ++q) {
-          segs.push_back({S[q].p0, S[q].n, S[q].row, S[q].slot, S[q].lane0, S[q].flags});
-          wave_nnz += S[q].n;
-          wave_rows += (S[q].flags & kSegLast) ? 1 : 0;
-        }
-      };
-      size_t i = 0;
-      while (i < S.size() && narrow(S[i])) {  // narrow: per grid window, cut by nonzeros
-        const uint32_t g = S[i].clo / St;
-        uint64_t nnz = 0;
-        size_t j = i;
-        const uint64_t cap = cap_nnz();
-        while (j < S.size() && narrow(S[j]) && S[j].clo / St == g && (j == i || nnz + S[j].n <= cap))
-          nnz += S[j++].n;
-        emit(i, j);
-        i = j;
-      }
-      while (i < S.size()) {  // wide: greedy, cut at the window width or ~cap nonzeros
-        const uint32_t xlo = S[i].clo / align * align;
-        uint32_t hi = S[i].chi;
-        uint64_t nnz = 0;
-        size_t j = i;
-        const uint64_t cap = cap_nnz();
-        while (j < S.size()) {
-          const uint32_t nhi = std::max(hi, S[j].chi);
-          if (j > i && (static_cast<uint64_t>(nhi) - xlo + 1 > W || nnz + S[j].n > cap)) break;
-          hi = nhi;
-          nnz += S[j].n;
-          ++j;
-        }
-        emit(i, j);
-        i = j;
-      }
-      if (w == 0 || h->fused_waves)
-        h->blk_tiles[k] += static_cast<uint32_t>(tiles.size() - tiles_before);
     }
-    h->wave_nnz[w] = wave_nnz;
-    h->wave_rows[w] = wave_rows;
-    if (h->fused_waves) {  // append to the single list: rebase the tiles' segment ranges
-      const uint32_t off = static_cast<uint32_t>(all_segs.size());
-      for (Tile& t : tiles) {
-        t.seg0 += off;
-        t.seg1 += off;
+    // windowed tiles.  Narrow segments (span <= A = W/3) are binned into a fixed grid of windows
+    // [g*St, g*St + W), stride St = W - A: a segment whose first column lies in [g*St, (g+1)*St)
+    // fits window g, so the rare wide segments (e.g. a row's clusters in two adjacent beams,
+    // merged into one segment) cannot cut the tiles of narrow ones short.  Wide segments are
+    // packed greedily in first-column order.  Each bin: first-column order, cut at ~cap nonzeros.
+    auto& S = win[w][k];
+    std::stable_sort(S.begin(), S.end(), [&](const HostSeg& a, const HostSeg& b) {
+      const bool na = narrow(a), nb = narrow(b);
+      if (na != nb) return na;
+      const uint32_t ga = na ? a.clo / St : 0, gb = nb ? b.clo / St : 0;
+      if (ga != gb) return ga < gb;
+      return a.clo != b.clo ? a.clo < b.clo : a.row < b.row;
+    });
+    auto emit = [&](size_t i, size_t j) {
+      uint32_t lo = S[i].clo, hi = S[i].chi;
+      for (size_t q = i; q < j; ++q) {
+        lo = std::min(lo, S[q].clo);
+        hi = std::max(hi, S[q].chi);
       }
-      all_tiles.insert(all_tiles.end(), tiles.begin(), tiles.end());
-      all_segs.insert(all_segs.end(), segs.begin(), segs.end());
-      all_rows += wave_rows;
-      if (w + 1 < h->n_waves) continue;
-      tiles.swap(all_tiles);
-      segs.swap(all_segs);
-      for (uint32_t v = 1; v < h->n_waves; ++v) h->wave_tiles[v] = 0;
-      h->fused_rows = all_rows;
-      h->fused_nnz = 0;
-      for (uint32_t v = 0; v < h->n_waves; ++v) h->fused_nnz += h->wave_nnz[v];
+      const uint32_t xlo = lo / align * align;
+      // longest segment first inside the tile (warps pull segments dynamically)
+      std::stable_sort(S.begin() + i, S.begin() + j,
+                       [](const HostSeg& a, const HostSeg& b) { return a.n > b.n; });
+      uint32_t xlen = (hi - xlo + 1 + align - 1) / align * align;
+      if (xlo + xlen > xcap) xlen = static_cast<uint32_t>(xcap - xlo);
+      tiles.push_back({xlo, static_cast<uint16_t>(xlen), blk, static_cast<uint32_t>(segs.size()),
+                       static_cast<uint32_t>(segs.size() + (j - i))});
+      for (size_t q = i; q < j; ++q) take(S[q]);
+    };
+    size_t i = 0;
+    while (i < S.size() && narrow(S[i])) {  // narrow: per grid window, cut by nonzeros
+      const uint32_t g = S[i].clo / St;
+      uint64_t nnz = 0;
+      size_t j = i;
+      const uint64_t cap = cap_nnz();
+      while (j < S.size() && narrow(S[j]) && S[j].clo / St == g && (j == i || nnz + S[j].n <= cap))
+        nnz += S[j++].n;
+      emit(i, j);
+      i = j;
     }
-    const uint32_t lw = h->fused_waves ? 0 : w;  // the fused list is uploaded as launch 0
+    while (i < S.size()) {  // wide: greedy, cut at the window width or ~cap nonzeros
+      const uint32_t xlo = S[i].clo / align * align;
+      uint32_t hi = S[i].chi;
+      uint64_t nnz = 0;
+      size_t j = i;
+      const uint64_t cap = cap_nnz();
+      while (j < S.size()) {
+        const uint32_t nhi = std::max(hi, S[j].chi);
+        if (j > i && (static_cast<uint64_t>(nhi) - xlo + 1 > W || nnz + S[j].n > cap)) break;
+        hi = nhi;
+        nnz += S[j].n;
+        ++j;
+      }
+      emit(i, j);
+      i = j;
+    }
+    if (blk != kNoBlock) h->blk_tiles[k] += static_cast<uint32_t>(tiles.size() - tiles_before);
+  }
+  for (uint32_t w = 0; w < NW; ++w) {
+    h->wave_nnz[w] = wnnz[w];
+    h->wave_rows[w] = wrows[w];
+    h->wave_tiles[w] = 0;
+  }
+  if (h->fused_waves) {
+    h->fused_rows = lrows[0];
+    h->fused_nnz = ldone[0];
+  }
+  for (uint32_t lw = 0; lw < NL; ++lw) {  // the fused list is uploaded as launch 0
+    const auto& tiles = ltiles[lw];
+    const auto& segs = lsegs[lw];
     h->wave_tiles[lw] = static_cast<uint32_t>(tiles.size());
-    if (!tiles.empty()) {
-      DG_CUDA(cudaMalloc(&h->d_tiles[lw], tiles.size() * sizeof(Tile)));
-      DG_CUDA(cudaMemcpy(h->d_tiles[lw], tiles.data(), tiles.size() * sizeof(Tile),
-                         cudaMemcpyHostToDevice));
-      DG_CUDA(cudaMalloc(&h->d_segs[lw], segs.size() * sizeof(Segment)));
-      DG_CUDA(cudaMemcpy(h->d_segs[lw], segs.data(), segs.size() * sizeof(Segment),
-                         cudaMemcpyHostToDevice));
-      h->plan_bytes += tiles.size() * sizeof(Tile) + segs.size() * sizeof(Segment);
-    }
+    if (tiles.empty()) continue;
+    DG_CUDA(cudaMalloc(&h->d_tiles[lw], tiles.size() * sizeof(Tile)));
+    DG_CUDA(cudaMemcpy(h->d_tiles[lw], tiles.data(), tiles.size() * sizeof(Tile),
+                       cudaMemcpyHostToDevice));
+    DG_CUDA(cudaMalloc(&h->d_segs[lw], segs.size() * sizeof(Segment)));
+    DG_CUDA(cudaMemcpy(h->d_segs[lw], segs.data(), segs.size() * sizeof(Segment),
+                       cudaMemcpyHostToDevice));
+    h->plan_bytes += tiles.size() * sizeof(Tile) + segs.size() * sizeof(Segment);
   }
   if (h->n_carry_slots) {
     const uint64_t n = h->n_carry_slots * 32;
