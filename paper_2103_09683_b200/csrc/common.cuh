@@ -63,10 +63,12 @@ struct SoA {
   __device__ __forceinline__ static V v_of(const Raw& r) { return r.v; }
   // a placeholder element for masked-off lanes: a valid column, value bits 0
   __device__ __forceinline__ static Raw filler(uint32_t col) { return {static_cast<I>(col), V(0)}; }
-  // L2 prefetch of the 128-byte lines of 256 positions starting at p: lanes [0, lc) take the
+  // L2 prefetch of the 128-byte lines of 32 * U positions starting at p: lanes [0, lc) take the
   // column lines, lanes [lc, lc + lv) the value lines
-  __device__ __forceinline__ void prefetch256(uint64_t p, uint32_t room, uint32_t lane) const {
-    constexpr uint32_t lc = 2 * sizeof(I), lv = 2 * sizeof(V);
+  template <int U>
+  __device__ __forceinline__ void prefetch_batch(uint64_t p, uint32_t room, uint32_t lane) const {
+    constexpr uint32_t lc = U * sizeof(I) / 4, lv = U * sizeof(V) / 4;
+    static_assert(lc + lv <= 32, "one line per lane");
     const char* a = nullptr;
     if (lane < lc) {
       if (lane * (128 / sizeof(I)) < room) a = reinterpret_cast<const char*>(col + p) + 128 * lane;
@@ -91,9 +93,10 @@ struct Packed16 {
   __device__ __forceinline__ static uint16_t c_of(Raw r) { return static_cast<uint16_t>(r >> 16); }
   __device__ __forceinline__ static uint16_t v_of(Raw r) { return static_cast<uint16_t>(r & 0xFFFFu); }
   __device__ __forceinline__ static Raw filler(uint32_t col) { return col << 16; }
-  // lines of positions [p, p + min(256, room)): no line past the segment is fetched
-  __device__ __forceinline__ void prefetch256(uint64_t p, uint32_t room, uint32_t lane) const {
-    if (lane < 8 && 32 * lane < room) asm volatile("prefetch.global.L2 [%0];" ::"l"(w + p + 32 * lane));
+  // lines of positions [p, p + min(32 * U, room)): no line past the segment is fetched
+  template <int U>
+  __device__ __forceinline__ void prefetch_batch(uint64_t p, uint32_t room, uint32_t lane) const {
+    if (lane < U && 32 * lane < room) asm volatile("prefetch.global.L2 [%0];" ::"l"(w + p + 32 * lane));
   }
 };
 

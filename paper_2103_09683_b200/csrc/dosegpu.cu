@@ -255,6 +255,8 @@ int launch_tiles(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t 
       case 11: return launch_tiles_cfg<M, Acc, 32, 8, 0, 0>(h, mat, x, y, s);
       case 12: return launch_tiles_cfg<M, Acc, 32, 8, 0, kP, 3>(h, mat, x, y, s);
       case 13: return launch_tiles_cfg<M, Acc, 32, 8, 0, kP, 4>(h, mat, x, y, s);
+      // (measured, rejected: wider batches U = 12 at 32 / 28 warps, U = 16 at 28 warps --
+      //  C2 2.70 / 2.66 / 2.82 ms vs 2.62; profiles/README.md)
       // (measured, rejected: cp.async.bulk.prefetch.L2 by one lane instead of per-line
       //  prefetches, P = 2/4/8 -- C2 2.94-3.00 ms vs 2.80; profiles/README.md)
       default:

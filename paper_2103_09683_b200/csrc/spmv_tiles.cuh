@@ -240,16 +240,15 @@ __device__ __forceinline__ uint32_t load_batch(const M& mat, typename M::Raw* r,
   return mask;
 }
 
-// L2 prefetch of batches [b, b + P) of segment s: lane l touches chunk l % 8 of batch b + l / 8.
+// L2 prefetch of batches [b, b + P) of segment s: lane l < U touches line l of each batch.
 // Prefetches hold no registers, so the stream runs P batches ahead of the register pipeline.
 template <int U, int P, class M>
 __device__ __forceinline__ void prefetch_batches(const M& mat, const SegRun& s, uint32_t b,
                                                  uint32_t lane) {
-  static_assert(U == 8, "prefetch granule is an 8-chunk (256-position) batch");
 #pragma unroll
   for (int k = 0; k < P; ++k) {
     const uint32_t rel = (b + k) * (32 * U);
-    if (rel < s.hi) mat.prefetch256(s.base0 + rel, s.hi - rel, lane);
+    if (rel < s.hi) mat.template prefetch_batch<U>(s.base0 + rel, s.hi - rel, lane);
   }
 }
 
@@ -260,17 +259,22 @@ template <int U, class M, typename Acc, class X>
 __device__ __forceinline__ void consume_batch(const typename M::Raw* r, uint32_t mask, const X& xr,
                                               Acc& acc) {
   using Ops = AccOps<Acc>;
-  Acc xv[U];
+  // wide batches gather x in groups of 8 (bounded live registers); U = 8 is one group
+  constexpr int G = U > 8 ? 4 : U;
 #pragma unroll
-  for (int u = 0; u < U; ++u) xv[u] = xr(M::c_of(r[u]));
-  if (mask == kFullMask<U>) {
+  for (int g = 0; g < U; g += G) {
+    Acc xv[G];
 #pragma unroll
-    for (int u = 0; u < U; ++u) acc = Ops::add(acc, Ops::prod(M::v_of(r[u]), xv[u]));
-  } else {
+    for (int u = 0; u < G; ++u) xv[u] = xr(M::c_of(r[g + u]));
+    if (mask == kFullMask<U>) {
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const Acc p = Ops::prod(M::v_of(r[u]), xv[u]);
-      acc = Ops::add(acc, (mask & (1u << u)) ? p : Acc(0));
+      for (int u = 0; u < G; ++u) acc = Ops::add(acc, Ops::prod(M::v_of(r[g + u]), xv[u]));
+    } else {
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        const Acc p = Ops::prod(M::v_of(r[g + u]), xv[u]);
+        acc = Ops::add(acc, (mask & (1u << (g + u))) ? p : Acc(0));
+      }
     }
   }
 }
