@@ -148,10 +148,12 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------- CPU baselines ------
-def cpu_reference_run(ps, sample_rows: int, reps: int, warmup: int) -> dict:
+def cpu_reference_run(ps, sample_rows: int, reps: int, warmup: int,
+                      target_s: float = 0.0) -> dict:
     """The reference's own CPU dose path, unmodified (oracle/_ref = /root/reference/proj built
     by oracle/Makefile): ddm::generate on a row sample of the workload's profile, then
-    ddm::run_bench(RowChunk, lane_width 32, workers = all host threads) -- bench.cpp:38-103."""
+    ddm::run_bench(RowChunk, lane_width 32, workers = all host threads) -- bench.cpp:38-103.
+    target_s > 0: reps chosen so the timed CPU work is about target_s seconds."""
     from oracle.oracle import Oracle, Profile, have_reference, traffic_bytes
     if len(ps) > 1 and len({p.cols for p in ps}) == 1 and ps[0].seed > 100:
         ps = ps[:1]  # C5: the scenarios are separate matrices; sample one of them
@@ -164,6 +166,10 @@ def cpu_reference_run(ps, sample_rows: int, reps: int, warmup: int) -> dict:
     parts = [orc.generate(p) for p in sub]
     m = parts[0] if len(parts) == 1 else hstack(parts)
     if kind == "reference":
+        if target_s > 0:  # calibrate on one evaluation
+            t1 = orc.run_bench(m, algorithm=1, lane_width=32, workers=cores, reps=1, warmup=1,
+                               vector_seed=42)["mean_seconds"]
+            reps = max(3, min(400, int(target_s / max(t1, 1e-6)) + 1))
         r = orc.run_bench(m, algorithm=1, lane_width=32, workers=cores, reps=reps,
                           warmup=warmup, vector_seed=42)
         mean_s = r["mean_seconds"]
@@ -380,22 +386,25 @@ def run_ours(args):
         # peer memory (CUDA IPC mappings), then a one-element all_reduce as the device-side
         # barrier that orders every rank's stores before the step ends
         from paper_2103_09683_b200.sharded import FusedGather
-        fg = FusedGather(engines[0], bounds, local)
-        flag = torch.zeros(1, dtype=torch.float64, device="cuda")
+        if FusedGather.preflight(local):  # same answer on every rank
+            fg = FusedGather(engines[0], bounds, local)
+            flag = torch.zeros(1, dtype=torch.float64, device="cuda")
 
-        def step_fused():
-            step()
-            dist.all_reduce(flag)
+            def step_fused():
+                step()
+                dist.all_reduce(flag)
 
-        for _ in range(2):
-            step_fused()
-        torch.cuda.synchronize()
-        dist.barrier()
-        fused_ms = timed(step_fused, e2e_steps)
-        dist.barrier()
-        assert torch.equal(fg.full.view(torch.int64), full[0].view(torch.int64)), \
-            "fused gather differs from the NCCL all-gather"
-        fg.close()
+            for _ in range(2):
+                step_fused()
+            torch.cuda.synchronize()
+            dist.barrier()
+            fused_ms = timed(step_fused, e2e_steps)
+            dist.barrier()
+            assert torch.equal(fg.full.view(torch.int64), full[0].view(torch.int64)), \
+                "fused gather differs from the NCCL all-gather"
+            fg.close()
+        else:
+            fused_ms = -1.0  # CUDA IPC unavailable between these processes: not measured
 
     model_bytes = sum(e.info["model_bytes"] for e in engines)
     nnz = sum(e.info["nnz"] for e in engines)
@@ -421,7 +430,7 @@ def run_ours(args):
     achieved = dom["bytes"] / (dom["ms"] * 1e-3) / 1e9
     traffic = None
     tf = os.path.join(ROOT, "profiles", "dram_bytes_per_launch.json")
-    if os.path.exists(tf):
+    if os.path.exists(tf) and world == 1 and not args.rows:  # profiled: the full 1-GPU workload
         try:
             traffic = json.load(open(tf)).get(f"{args.config}:{args.accum}:{dom_name}")
         except Exception:
@@ -464,7 +473,8 @@ def run_ours(args):
                 "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": sum(int(e.info["n_kernels"]) for e in engines) * args.steps * world,
         "ms_per_step_gathered": (gather_ms / e2e_steps) if gather_ms else None,
-        "ms_per_step_gathered_fused": (fused_ms / e2e_steps) if fused_ms else None,
+        "ms_per_step_gathered_fused": (fused_ms / e2e_steps) if fused_ms > 0 else
+                                      ("unavailable: CUDA IPC" if fused_ms < 0 else None),
         "clocks": clk,
     }
     if args.config == "c5":
@@ -487,7 +497,7 @@ def run_ours(args):
         engines = fengs
     if world == 1 and not args.no_cpu_baseline:
         try:
-            r = cpu_reference_run(ps, args.cpu_sample_rows, 5, 1)
+            r = cpu_reference_run(ps, args.cpu_sample_rows, 5, 1, target_s=10.0)
             line["cpu_baseline"] = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as ex:  # reported, never silently replaced
             line["cpu_baseline"] = {"value": None, "error": str(ex)[:200]}

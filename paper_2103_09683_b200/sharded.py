@@ -136,6 +136,42 @@ class FusedGather:
         engine.set_gather_targets(ptrs)
         self.full = self.mine.tensor()
 
+    @staticmethod
+    def preflight(device: int, group=None) -> bool:
+        """Whether every rank can export and map CUDA IPC buffers (the same answer on every rank:
+        a failure on one rank must not leave the others blocked in a collective).  Allocates,
+        exchanges and maps a one-element buffer per rank."""
+        import torch
+        import torch.distributed as dist
+
+        from .dose import PeerBuffer
+
+        mine, handle = None, None
+        try:
+            mine = PeerBuffer(1, device)
+            handle = mine.handle
+        except Exception:
+            handle = None
+        handles = [None] * dist.get_world_size(group)
+        dist.all_gather_object(handles, handle, group=group)
+        me = dist.get_rank(group)
+        ok, opened = all(h is not None for h in handles), []
+        if ok:
+            try:
+                opened = [PeerBuffer.open(h, 1, device) for g, h in enumerate(handles) if g != me]
+            except Exception:
+                ok = False
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=f"cuda:{device}")
+        if dist.get_backend(group) == "gloo":
+            flag = flag.cpu()
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        for p in opened:
+            p.close()
+        dist.barrier(group=group)
+        if mine is not None:
+            mine.close()
+        return bool(flag.item())
+
     def dose(self, x, y_local, *, stream: int = 0):
         """This rank's slice into y_local and into every rank's full d; returns this rank's full
         d once every rank has finished (stream sync + barrier)."""
