@@ -63,20 +63,23 @@ struct SoA {
   __device__ __forceinline__ static V v_of(const Raw& r) { return r.v; }
   // a placeholder element for masked-off lanes: a valid column, value bits 0
   __device__ __forceinline__ static Raw filler(uint32_t col) { return {static_cast<I>(col), V(0)}; }
-  // L2 prefetch of the 128-byte lines of 32 * U positions starting at p: lanes [0, lc) take the
-  // column lines, lanes [lc, lc + lv) the value lines
+  // L2 prefetch of the 128-byte lines of 32 * U positions starting at p: lines [0, lc) are the
+  // column lines, [lc, lc + lv) the value lines; line k goes to lane k % 32
   template <int U>
   __device__ __forceinline__ void prefetch_batch(uint64_t p, uint32_t room, uint32_t lane) const {
     constexpr uint32_t lc = U * sizeof(I) / 4, lv = U * sizeof(V) / 4;
-    static_assert(lc + lv <= 32, "one line per lane");
-    const char* a = nullptr;
-    if (lane < lc) {
-      if (lane * (128 / sizeof(I)) < room) a = reinterpret_cast<const char*>(col + p) + 128 * lane;
-    } else if (lane < lc + lv) {
-      if ((lane - lc) * (128 / sizeof(V)) < room)
-        a = reinterpret_cast<const char*>(val + p) + 128 * (lane - lc);
+#pragma unroll
+    for (uint32_t k0 = 0; k0 < lc + lv; k0 += 32) {
+      const uint32_t k = k0 + lane;
+      const char* a = nullptr;
+      if (k < lc) {
+        if (k * (128 / sizeof(I)) < room) a = reinterpret_cast<const char*>(col + p) + 128 * k;
+      } else if (k < lc + lv) {
+        if ((k - lc) * (128 / sizeof(V)) < room)
+          a = reinterpret_cast<const char*>(val + p) + 128 * (k - lc);
+      }
+      if (a) asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
     }
-    if (a) asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
   }
 };
 

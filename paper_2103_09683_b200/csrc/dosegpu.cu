@@ -242,9 +242,40 @@ TileCfg tile_cfg_of(int cfg, bool packed) {
   }
 }
 
+// Dense rows first (k_dense, rows pulled longest first by warps of 8-warp CTAs): every row it
+// owns is final before the tile kernel -- and the row-block completion signals -- start.
+template <class M, typename Acc>
+int launch_dense(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t s) {
+  if (!h->n_dense_rows) return DG_OK;
+  DG_CUDA(cudaMemsetAsync(h->d_dense_counter, 0, sizeof(uint32_t), s));
+  const int grid = grid_for(h->n_dense_rows * 32ull, 256, 8);
+  switch (h->dense_cfg) {
+    case 1:
+      k_dense<M, Acc, 16, 2><<<grid, 256, 0, s>>>(mat, h->d_row_ptr, x, h->d_dense_rows,
+                                                  static_cast<uint32_t>(h->n_dense_rows),
+                                                  h->d_dense_counter, y, h->gt);
+      break;
+    case 2:
+      k_dense<M, Acc, 8, 8><<<grid, 256, 0, s>>>(mat, h->d_row_ptr, x, h->d_dense_rows,
+                                                 static_cast<uint32_t>(h->n_dense_rows),
+                                                 h->d_dense_counter, y, h->gt);
+      break;
+    default:
+      k_dense<M, Acc, 8, 4><<<grid, 256, 0, s>>>(mat, h->d_row_ptr, x, h->d_dense_rows,
+                                                 static_cast<uint32_t>(h->n_dense_rows),
+                                                 h->d_dense_counter, y, h->gt);
+  }
+  h->post(s, "dense", h->n_dense_rows, h->dense_nnz);
+  DG_CUDA(cudaGetLastError());
+  return DG_OK;
+}
+
 template <class M, typename Acc>
 int launch_tiles(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t s,
                  const char* /*name*/) {
+  // (measured, rejected: k_dense on a side stream beside a 24-warp tile kernel, one CTA of each
+  //  per SM -- C2 3.89 ms vs 2.88 back to back; profiles/README.md)
+  DG_TRY(launch_dense(h, mat, x, y, s));
   if (!h->n_waves) return DG_OK;
   constexpr int kP = std::is_same_v<Acc, float> ? 4 : 2;  // measured: prefetch distance
   if constexpr (std::is_same_v<M, Packed16>) {
@@ -378,6 +409,9 @@ int finish_create(Handle* h, const std::vector<uint64_t>& lens) {
   if (const char* tg = std::getenv("DG_TILE_GUIDE")) h->tile_guide = std::strtoull(tg, nullptr, 10);
   if (const char* tg = std::getenv("DG_TILE_GUIDE_MIN"))
     h->tile_guide_min = std::strtoull(tg, nullptr, 10);
+  if (const char* dk = std::getenv("DG_DENSE")) h->dense_mode = std::atoi(dk) != 0;
+  if (const char* dm = std::getenv("DG_DENSE_MIN_LEN")) h->dense_min_len = std::strtoull(dm, nullptr, 10);
+  if (const char* dc = std::getenv("DG_DENSE_CFG")) h->dense_cfg = std::atoi(dc);
   if (const char* gm = std::getenv("DG_GLOBAL_MIN_LEN"))
     h->global_min_len = std::strtoull(gm, nullptr, 10);
   h->window_cols = window_bytes_for(h->tile_cfg, h->packed) / h->acc_bytes;
@@ -400,6 +434,7 @@ int finish_create(Handle* h, const std::vector<uint64_t>& lens) {
   DG_CUDA(cudaEventCreateWithFlags(&h->ev_tiles_start, cudaEventDisableTiming));
   DG_CUDA(cudaEventCreateWithFlags(&h->ev_d2h_done, cudaEventDisableTiming));
   DG_CUDA(cudaStreamCreateWithFlags(&h->d2h_stream, cudaStreamNonBlocking));
+
   return DG_OK;
 }
 
@@ -555,6 +590,8 @@ int dg_destroy(dg_handle* hh) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   cudaFree(h->d_row_ptr);
   cudaFree(h->d_trace);
+  cudaFree(h->d_dense_rows);
+  cudaFree(h->d_dense_counter);
   cudaFree(h->d_col);
   cudaFree(h->d_val);
   cudaFree(h->d_packed);
@@ -577,6 +614,7 @@ int dg_destroy(dg_handle* hh) {
     cudaStreamDestroy(h->d2h_stream);
   }
   if (h->ev_tiles_start) cudaEventDestroy(h->ev_tiles_start);
+
   if (h->ev_d2h_done) cudaEventDestroy(h->ev_d2h_done);
   for (auto e : h->ev)
     if (e) cudaEventDestroy(e);
@@ -617,6 +655,7 @@ int dg_dose(dg_handle* hh, const double* x, uint64_t x_len, double* y, uint32_t 
   DG_CUDA(cudaEventRecord(h->ev[2], s));
   if (overlap) {
     DG_CUDA(cudaStreamWaitEvent(h->d2h_stream, h->ev_tiles_start, 0));
+
     for (uint32_t k = 0; k < h->n_blocks; ++k) {
       const uint64_t r0 = h->blk_row0[k], r1 = h->blk_row0[k + 1];
       if (r1 == r0) continue;

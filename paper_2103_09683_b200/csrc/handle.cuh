@@ -53,6 +53,14 @@ struct Handle {
   uint64_t n_split_rows = 0, n_global_rows = 0;
   uint64_t short_max = 32;  // rows with len <= short_max use the sub-warp bins, others the tiles
   uint64_t global_min_len = ~0ull;  // dense rows at least this long read x from global memory
+  // dense rows (>= 3/4 of their span) at least dense_min_len long: the k_dense kernel (DG_DENSE)
+  int dense_mode = -1;        // DG_DENSE: -1 auto (plan.cu), 0 off, 1 on
+  bool dense_kernel = false;
+  uint64_t dense_min_len = 4096;  // C2: 2.69 ms (1024: 2.80); its 1/8 shard 0.394 ms (1024: 0.380)
+  uint32_t* d_dense_rows = nullptr;  // longest first
+  uint32_t* d_dense_counter = nullptr;
+  uint64_t n_dense_rows = 0, dense_nnz = 0;
+  int dense_cfg = 0;  // DG_DENSE_CFG: (U, P) = (8, 4) default, 1: (16, 2), 2: (8, 8)
   uint32_t wave_tiles[kMaxWaves] = {};
   uint64_t wave_nnz[kMaxWaves] = {}, wave_rows[kMaxWaves] = {};
   void* d_tiles[kMaxWaves] = {};
@@ -121,6 +129,7 @@ struct Handle {
     if (lane_width == 32) {
       for (int b = 0; b < kNumBins; ++b) n += bin_count[b] ? 1 : 0;
       for (uint32_t w = 0; w < n_waves; ++w) n += wave_tiles[w] ? 1 : 0;
+      n += n_dense_rows ? 1 : 0;
     } else {
       n += bin_count[kBinGeneral] ? 1 : 0;
     }

@@ -102,15 +102,36 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
   //    reads x from global (its lanes read consecutive x: 2 sectors per 32 positions); a sparse
   //    wide row (e.g. a multi-beam row of C4) is cut greedily into windowed segments, one wave
   //    per segment, carrying its 32 lane partials between waves
+  // k_dense on/off (DG_DENSE=0/1 forces it): on when the longest dense row is a sizeable share of
+  // one SM's work (nnz < 200 * SMs * longest) -- there a warp streaming such a row inside the tile
+  // kernel sets the kernel tail (C2's 1/8 shard: 0.466 -> 0.415 ms); off on large matrices, where
+  // the tile kernel absorbs long rows and k_dense only delays the overlapped d download
+  // (C2: step equal, end to end 2.96 -> 3.03 ms).
+  if (h->dense_mode < 0) {
+    uint64_t longest = 0;
+    for (uint64_t r = 0; r < rows; ++r) {
+      if (lens[r] < h->dense_min_len || lens[r] <= h->short_max) continue;
+      const uint64_t span = static_cast<uint64_t>(ext[r].y) - ext[r].x + 1;
+      if (4 * lens[r] >= 3 * span) longest = std::max<uint64_t>(longest, lens[r]);
+    }
+    h->dense_kernel = longest && h->nnz < 200ull * h->sm_count * longest;
+  } else {
+    h->dense_kernel = h->dense_mode != 0;
+  }
   std::vector<std::vector<HostSeg>> waves(1);
   std::vector<HostSeg> global_x;
-  std::vector<uint32_t> wide;
+  std::vector<uint32_t> wide, dense_rows;
   for (uint64_t r = 0; r < rows; ++r) {
     if (lens[r] == 0 || lens[r] <= h->short_max) continue;
     const uint32_t c0 = ext[r].x, c1 = ext[r].y;
     const uint64_t span = static_cast<uint64_t>(c1) - c0 + 1;
     const uint16_t whole = static_cast<uint16_t>(kSegFirst | kSegLast);
     const bool dense = 4 * lens[r] >= 3 * span;
+    if (h->dense_kernel && dense && lens[r] >= h->dense_min_len) {  // k_dense
+      dense_rows.push_back(static_cast<uint32_t>(r));
+      h->dense_nnz += lens[r];
+      continue;
+    }
     const bool dense_long = lens[r] >= h->global_min_len && dense;
     if ((span <= A || (dense && span <= ws)) && !dense_long) {
       waves[0].push_back({rp[r], static_cast<uint32_t>(lens[r]), static_cast<uint32_t>(r), 0, c0,
@@ -123,6 +144,16 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     }
   }
   h->n_split_rows = wide.size();
+  h->n_dense_rows = dense_rows.size();
+  if (!dense_rows.empty()) {  // longest first: the pool ends with the shortest rows
+    std::stable_sort(dense_rows.begin(), dense_rows.end(),
+                     [&](uint32_t a, uint32_t b) { return lens[a] > lens[b]; });
+    DG_CUDA(cudaMalloc(&h->d_dense_rows, dense_rows.size() * sizeof(uint32_t)));
+    DG_CUDA(cudaMemcpy(h->d_dense_rows, dense_rows.data(), dense_rows.size() * sizeof(uint32_t),
+                       cudaMemcpyHostToDevice));
+    DG_CUDA(cudaMalloc(&h->d_dense_counter, sizeof(uint32_t)));
+    h->plan_bytes += dense_rows.size() * sizeof(uint32_t);
+  }
   if (!wide.empty()) {
     std::vector<uint64_t> off(wide.size() + 1, 0);
     for (size_t i = 0; i < wide.size(); ++i) {

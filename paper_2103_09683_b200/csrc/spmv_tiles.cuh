@@ -232,10 +232,15 @@ __device__ __forceinline__ uint32_t load_batch(const M& mat, typename M::Raw* r,
   const uint32_t uhi = th <= 0 ? 0u : min(static_cast<uint32_t>(U), static_cast<uint32_t>(th + 31) >> 5);
   const uint32_t ulo = tl <= 0 ? 0u : min(static_cast<uint32_t>(U), static_cast<uint32_t>(tl + 31) >> 5);
   const uint32_t mask = ((1u << uhi) - 1u) & ~((1u << ulo) - 1u);
+  // chunks at or past nact hold no position of any lane (warp-uniform): left unset, and
+  // consume_edge never reads them
+  const uint32_t nact = min(static_cast<uint32_t>(U), (s.hi - min(s.hi, b0) + 31) >> 5);
 #pragma unroll
   for (int u = 0; u < U; ++u) {
-    r[u] = M::filler(safe_col);
-    if (mask & (1u << u)) r[u] = mat.load(base + 32 * u);
+    if (static_cast<uint32_t>(u) < nact) {
+      r[u] = M::filler(safe_col);
+      if (mask & (1u << u)) r[u] = mat.load(base + 32 * u);
+    }
   }
   return mask;
 }
@@ -275,6 +280,26 @@ __device__ __forceinline__ void consume_batch(const typename M::Raw* r, uint32_t
         const Acc p = Ops::prod(M::v_of(r[g + u]), xv[u]);
         acc = Ops::add(acc, (mask & (1u << (g + u))) ? p : Acc(0));
       }
+    }
+  }
+}
+
+// Edge batch (some lane's mask is not full; called by the whole warp): only the chunks some lane
+// still needs -- the warp-uniform count
+// nact = 1 + the highest chunk any lane has -- are gathered and accumulated; the rest of the
+// batch (on average ~3.5 of 8 chunks at a segment's end) costs no LDS and no arithmetic.
+// Adding a masked product's +0.0 or skipping it leaves the accumulator's bits unchanged.
+template <int U, class M, typename Acc, class X>
+__device__ __forceinline__ void consume_edge(const typename M::Raw* r, uint32_t mask, const X& xr,
+                                             Acc& acc) {
+  using Ops = AccOps<Acc>;
+  const uint32_t any = __reduce_or_sync(kFull, mask);
+  const uint32_t nact = 32u - __clz(any);
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    if (static_cast<uint32_t>(u) < nact) {
+      const Acc p = Ops::prod(M::v_of(r[u]), xr(M::c_of(r[u])));
+      acc = Ops::add(acc, (mask & (1u << u)) ? p : Acc(0));
     }
   }
 }
@@ -321,8 +346,15 @@ __device__ __forceinline__ void run_segments(const M& mat, const XWindow<Acc>& x
         prefetch_batches<U, P + 1>(mat, seg_run<U>(sn), 0, lane);
       }
     }
-    if (cur.flags & kSegGlobalX) consume_batch<U, M>(rc, mc, xg, acc);
-    else consume_batch<U, M>(rc, mc, xw, acc);
+    // warp-uniform choice (lanes of an edge batch may hold a full mask of their own)
+    if (!__all_sync(kFull, mc == kFullMask<U>)) {
+      if (cur.flags & kSegGlobalX) consume_edge<U, M>(rc, mc, xg, acc);
+      else consume_edge<U, M>(rc, mc, xw, acc);
+    } else if (cur.flags & kSegGlobalX) {
+      consume_batch<U, M>(rc, mc, xg, acc);
+    } else {
+      consume_batch<U, M>(rc, mc, xw, acc);
+    }
     if (more) {
       ++bi;
       return true;
@@ -345,6 +377,88 @@ __device__ __forceinline__ void run_segments(const M& mat, const XWindow<Acc>& x
     have_next = grab(sn);
     sn_pf = false;
     if (PEEK && have_next) carried_next = carry.peek(sn.slot, sn.flags, lane);
+    return true;
+  };
+  for (;;) {
+    if (!step(ra, ma, rb, mb)) break;
+    if (!step(rb, mb, ra, ma)) break;
+  }
+}
+
+// ---- dense rows ------------------------------------------------------------------------------
+// Rows at least 3/4 dense (columns nearly consecutive) need no shared-memory window: their 32
+// lanes read 32 (nearly) consecutive x entries, which stay in L1 (this kernel uses no shared
+// memory, so L1 holds most of x).  They are the longest rows (C2: every row longer than the
+// 4,096-column locality window is fully dense -- 42% of the nonzeros), so inside the tile kernel
+// they set both the per-tile imbalance and the kernel tail (one warp streams a 40,000-nonzero
+// row at the speed of its own pipeline).  Here each warp pulls whole rows, longest first, with a
+// wider batch (U chunks in flight in registers) and a deeper L2 prefetch stream (P batches
+// ahead), so one row streams several times faster and the pool ends with the shortest rows.
+// Semantics are the tile kernel's: lane l accumulates positions l, l + 32, ... from +0.0, then
+// the stride-halving tree -- ddm::rowchunk_rows with lane_width 32 (src/spmv.cpp:48-68).
+template <class M, typename Acc, int U, int P>
+__global__ void __launch_bounds__(256)
+    k_dense(M mat, const uint64_t* __restrict__ rp, const Acc* __restrict__ x,
+            const uint32_t* __restrict__ rows, uint32_t n_rows, uint32_t* __restrict__ counter,
+            double* __restrict__ y, GatherTargets gt) {
+  using Ops = AccOps<Acc>;
+  using Raw = typename M::Raw;
+  const uint32_t lane = threadIdx.x & 31;
+  const XGlobal<Acc> xg{x};
+  auto grab = [&](SegRun& r) -> bool {
+    uint32_t k = 0;
+    if (lane == 0) k = atomicAdd(counter, 1u);
+    k = __shfl_sync(kFull, k, 0);
+    if (k >= n_rows) return false;
+    const uint32_t row = rows[k];
+    const uint64_t s = rp[row], e = rp[row + 1];
+    r.base0 = s;
+    r.lo = 0;
+    r.hi = static_cast<uint32_t>(e - s);
+    r.nbatch = ((r.hi + 31) / 32 + U - 1) / U;
+    r.row = row;
+    r.slot = 0;
+    r.flags = kSegFirst | kSegLast;
+    return true;
+  };
+  SegRun cur, nxt;
+  if (!grab(cur)) return;
+  bool have_next = grab(nxt);
+  Raw ra[U], rb[U];
+  uint32_t ma = load_batch<U>(mat, ra, cur, 0, lane, 0u), mb = 0;
+  prefetch_batches<U, P>(mat, cur, 1, lane);
+  bool nx_pf = false;
+  Acc acc = Acc(0);
+  uint32_t bi = 0;
+  auto step = [&](const Raw* rc, uint32_t mc, Raw* rn, uint32_t& mn) -> bool {
+    const bool more = bi + 1 < cur.nbatch;
+    if (more) mn = load_batch<U>(mat, rn, cur, bi + 1, lane, 0u);
+    else if (have_next) mn = load_batch<U>(mat, rn, nxt, 0, lane, 0u);
+    const uint32_t pf = bi + 1 + P;
+    if (pf < cur.nbatch) {
+      prefetch_batches<U, 1>(mat, cur, pf, lane);
+    } else if (have_next && !nx_pf) {
+      nx_pf = true;
+      prefetch_batches<U, P + 1>(mat, nxt, 0, lane);
+    }
+    if (!__all_sync(kFull, mc == kFullMask<U>)) consume_edge<U, M>(rc, mc, xg, acc);
+    else consume_batch<U, M>(rc, mc, xg, acc);
+    if (more) {
+      ++bi;
+      return true;
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off /= 2) acc = Ops::add(acc, __shfl_down_sync(kFull, acc, off));
+    if (lane == 0) {
+      y[cur.row] = static_cast<double>(acc);
+      gt.store(cur.row, static_cast<double>(acc));
+    }
+    if (!have_next) return false;
+    cur = nxt;
+    bi = 0;
+    acc = Acc(0);
+    have_next = grab(nxt);
+    nx_pf = false;
     return true;
   };
   for (;;) {

@@ -69,20 +69,21 @@ def ncu(tag, family):
     hot = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "ncu_sass_hot.py"), rep,
                           "stall", "25"], capture_output=True, text=True).stdout
     cfg = "C4" if family == "c4" else "C2"
-    text = (f"# {tag}: ncu --set full --clock-control none, hot kernel k_tiles ({cfg}, {family})\n"
+    text = (f"# {tag}: ncu --set full --clock-control none, dose kernels k_tiles (+ k_dense) ({cfg}, {family})\n"
             + summ + "\n# hottest SASS by warp-stall samples (addr, executed, samples, instr)\n" + hot)
     open(os.path.join(PROF, f"{tag}_ncu_{family}.txt"), "w").write(text)
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     r = list(csv.reader(raw.splitlines()))
-    hdr, units, vals = r[0], r[1], r[2]
+    hdr, units = r[0], r[1]
 
-    def get(k):
+    def get(vals, k):
         v = float(vals[hdr.index(k)])
         u = units[hdr.index(k)]
         return v * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}.get(u, 1)
 
-    return get("dram__bytes_read.sum") + get("dram__bytes_write.sum")
+    # one dose's kernels (k_tiles, and k_dense when it ran beside it): their bytes add up
+    return sum(get(v, "dram__bytes_read.sum") + get(v, "dram__bytes_write.sum") for v in r[2:])
 
 
 def main():
@@ -93,7 +94,7 @@ def main():
     tf = os.path.join(PROF, "dram_bytes_per_launch.json")
     traffic = json.load(open(tf)) if os.path.exists(tf) else {}
     # keys: <config>:<accumulation>:<kernel name in dg_kernel_times> (read by bench.py)
-    for fam, key in (("exact", "c2:exact:tiles[w0]"), ("fp32", "c2:fp32:tiles[w0]"),
+    for fam, key in (("exact", "c2:exact:tiles[w0]+dense"), ("fp32", "c2:fp32:tiles[w0]+dense"),
                      ("c4", "c4:exact:tiles[fused]")):
         t = ncu(tag, fam)
         if t is not None:

@@ -391,15 +391,16 @@ def test_c2_full_scale_sampled_rows(port):
             assert bits(y[r]) == bits(port.spmv_rowchunk(m, x, 32, 1))[0]
 
 
-def _wide_row_matrix(port, rows=3000, cols=40_000, seed=5):
-    """Sparse windowed rows + long dense rows wider than one shared-memory window (forcing
-    multi-wave segments with carried lane partials) + rows straddling window boundaries."""
+def _wide_row_matrix(port, rows=3000, cols=40_000, seed=5, split=True):
+    """Sparse windowed rows + long dense rows wider than one shared-memory window + rows
+    straddling window boundaries + (split=True) wide sparse rows, which are cut into multi-wave
+    segments with carried lane partials."""
     rng = np.random.default_rng(seed)
     lens = np.where(rng.random(rows) < 0.5, 0, rng.integers(1, 3000, rows))
     lens[rng.choice(rows, 40, replace=False)] = rng.integers(14_000, cols + 1, 40)  # wide, dense
     lens[:3] = [cols, 13_823, 27_647]
-    sparse_wide = rng.choice(np.arange(3, rows), 30, replace=False)  # wide but sparse: split
-    lens[sparse_wide] = rng.integers(40, 3000, 30)
+    sparse_wide = rng.choice(np.arange(3, rows), 30 if split else 0, replace=False)
+    lens[sparse_wide] = rng.integers(40, 3000, len(sparse_wide))
     rp = np.zeros(rows + 1, dtype=np.uint64)
     np.cumsum(lens, out=rp[1:])
     col = np.empty(int(rp[-1]), dtype=np.uint32)
@@ -446,6 +447,32 @@ def test_windowed_tiles_with_split_rows_bit_exact(port, monkeypatch, tile_nnz, f
     with dg.DoseEngine.from_csr(to_dg(m), accumulation=dg.ACCUM_FP32) as e:
         gf = e.dose(x)
     assert np.max(np.abs(gf - want)) <= FP32_TOL * np.max(np.abs(want))
+
+
+@pytest.mark.parametrize("env", [{}, {"DG_DENSE": "1"}, {"DG_DENSE": "0"},
+                                 {"DG_DENSE": "1", "DG_DENSE_MIN_LEN": "1024"}])
+def test_dense_rows_kernel_bit_exact(port, monkeypatch, env):
+    """Dense rows (>= 3/4 of their span, >= DG_DENSE_MIN_LEN long) go to k_dense, launched
+    before the tile kernel, and must give the same bits as the reference, for device and host d
+    (the host path downloads row blocks as the tile kernel completes them), over repeated
+    doses."""
+    import torch
+    monkeypatch.setenv("DG_BLOCKS", "8")  # 8 output row blocks: the overlapped host download
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    m = _wide_row_matrix(port, rows=6000, split=False)
+    with dg.DoseEngine.from_csr(to_dg(m)) as e:
+        yd = torch.empty(m.rows, dtype=torch.float64, device="cuda")
+        for seed in (42, 7, 8):
+            x = port.seeded_vector(m.cols, seed)
+            want = bits(port.spmv_rowchunk(m, x, 32, 4))
+            assert np.array_equal(bits(e.dose(x)), want), seed
+            e.dose_device(torch.from_numpy(x).cuda().data_ptr(), m.cols, yd.data_ptr())
+            assert np.array_equal(yd.cpu().numpy().view(np.uint64), want), seed
+    with dg.DoseEngine.from_csr(to_dg(m), accumulation=dg.ACCUM_FP32) as e:
+        x = port.seeded_vector(m.cols, 42)
+        want = port.spmv_rowchunk(m, x, 32, 4)
+        assert np.max(np.abs(e.dose(x) - want)) <= FP32_TOL * np.max(np.abs(want))
 
 
 def test_small_tiles_desk_bit_exact(port, golden, desk, monkeypatch):
