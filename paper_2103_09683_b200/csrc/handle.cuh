@@ -79,7 +79,7 @@ struct Handle {
 
   // output row blocks (plan.cu): the d download of block k overlaps the kernel's later blocks
   static constexpr uint32_t kMaxBlocks = 64;     // DG_BLOCKS range
-  static constexpr uint32_t kDefaultBlocks = 8;
+  static constexpr uint32_t kDefaultBlocks = 32;  // C2: device step unchanged vs 8, e2e 2.87 -> 2.81
   uint32_t n_blocks = 1;
   uint64_t blk_row0[kMaxBlocks + 1] = {};
   uint32_t blk_tiles[kMaxBlocks] = {};

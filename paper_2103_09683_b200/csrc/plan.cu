@@ -107,14 +107,19 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
   // kernel sets the kernel tail (C2's 1/8 shard: 0.466 -> 0.415 ms); off on large matrices, where
   // the tile kernel absorbs long rows and k_dense only delays the overlapped d download
   // (C2: step equal, end to end 2.96 -> 3.03 ms).
+  // It also needs the dense rows to be >= 5% of the nonzeros: a handful of long rows (C1 has one
+  // or two) cost the tile kernel little and a separate launch more.
   if (h->dense_mode < 0) {
-    uint64_t longest = 0;
+    uint64_t longest = 0, dnnz = 0;
     for (uint64_t r = 0; r < rows; ++r) {
       if (lens[r] < h->dense_min_len || lens[r] <= h->short_max) continue;
       const uint64_t span = static_cast<uint64_t>(ext[r].y) - ext[r].x + 1;
-      if (4 * lens[r] >= 3 * span) longest = std::max<uint64_t>(longest, lens[r]);
+      if (4 * lens[r] >= 3 * span) {
+        longest = std::max<uint64_t>(longest, lens[r]);
+        dnnz += lens[r];
+      }
     }
-    h->dense_kernel = longest && h->nnz < 200ull * h->sm_count * longest;
+    h->dense_kernel = longest && h->nnz < 200ull * h->sm_count * longest && 20 * dnnz >= h->nnz;
   } else {
     h->dense_kernel = h->dense_mode != 0;
   }
@@ -224,7 +229,12 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
   // wave) by default.  Measured on C4: a short lag (64 blocks, lag 1 or 3, meant to read carried
   // partials back while still in L2) makes segments wait on tiles still in flight -- ~296 tiles
   // (2 per SM) of ~1M nonzeros are always in flight -- 7.95 / 6.83 ms vs 6.70 wave after wave.
-  uint32_t K = h->nnz >= (16ull << 20) ? Handle::kDefaultBlocks : 1;
+  // (~2 MB of d per block: the last block's download after the kernel is short, and small
+  // matrices do not pay 32 copies -- C1's end to end went 0.32 -> 0.51 ms at 32 blocks)
+  uint32_t K = h->nnz >= (16ull << 20)
+                   ? static_cast<uint32_t>(std::max<uint64_t>(
+                         1, std::min<uint64_t>(Handle::kDefaultBlocks, rows * 8 / (2u << 20))))
+                   : 1;
   if (const char* kb = std::getenv("DG_BLOCKS"))
     K = std::max<uint32_t>(1, std::min<uint32_t>(Handle::kMaxBlocks, std::atoi(kb)));
   uint32_t lag = K - 1;

@@ -588,6 +588,11 @@ constexpr size_t ring_smem_bytes() {
 
 // Persistent: one CTA per SM; dynamic smem = 2 * wcap * sizeof(Acc) (two x-window buffers)
 // + ring_smem_bytes<WARPS, R>() (R > 0: TMA-streamed matrix, Packed16 only).
+#ifndef DG_PREFETCH_SEGS
+#define DG_PREFETCH_SEGS 1
+#endif
+constexpr bool kPrefetchSegs = DG_PREFETCH_SEGS;
+
 template <class M, typename Acc, int WARPS, int U, int R = 0, int P = 0, int NB = 2,
           bool CARRY = true>
 __global__ void __launch_bounds__(WARPS * 32, 1)
@@ -622,6 +627,14 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       char* dst = reinterpret_cast<char*>(xbuf0 + b * wcap);
       for (uint32_t off = 0; off < bytes; off += 32768u)
         tma_load_1d(dst + off, src + off, min(32768u, bytes - off), &full[b]);
+      // the tile's segment descriptors into L2 (one bulk prefetch): the warps' grabs then wait
+      // on an L2 hit, not DRAM -- short segments need the next descriptor almost at once
+      const uint64_t sb = reinterpret_cast<uint64_t>(segs + T.seg0) & ~15ull;
+      const uint64_t se = (reinterpret_cast<uint64_t>(segs + T.seg1) + 15) & ~15ull;
+      if (kPrefetchSegs && se > sb)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sb),
+                     "r"(static_cast<uint32_t>(se - sb))
+                     : "memory");
     } else {
       mbar_arrive(&full[b]);  // terminal: completes the phase with tile_of[b] >= n_tiles
     }
