@@ -593,6 +593,7 @@ constexpr size_t ring_smem_bytes() {
 #endif
 constexpr bool kPrefetchSegs = DG_PREFETCH_SEGS;
 
+
 template <class M, typename Acc, int WARPS, int U, int R = 0, int P = 0, int NB = 2,
           bool CARRY = true>
 __global__ void __launch_bounds__(WARPS * 32, 1)
