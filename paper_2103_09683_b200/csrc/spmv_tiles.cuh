@@ -215,6 +215,7 @@ __device__ __forceinline__ SegRun seg_run(const Segment& S) {
 template <int U>
 constexpr uint32_t kFullMask = (1u << U) - 1u;
 
+
 template <int U, class M>
 __device__ __forceinline__ uint32_t load_batch(const M& mat, typename M::Raw* r, const SegRun& s,
                                                uint32_t b, uint32_t lane, uint32_t safe_col) {
@@ -232,15 +233,13 @@ __device__ __forceinline__ uint32_t load_batch(const M& mat, typename M::Raw* r,
   const uint32_t uhi = th <= 0 ? 0u : min(static_cast<uint32_t>(U), static_cast<uint32_t>(th + 31) >> 5);
   const uint32_t ulo = tl <= 0 ? 0u : min(static_cast<uint32_t>(U), static_cast<uint32_t>(tl + 31) >> 5);
   const uint32_t mask = ((1u << uhi) - 1u) & ~((1u << ulo) - 1u);
-  // chunks at or past nact hold no position of any lane (warp-uniform): left unset, and
-  // consume_edge never reads them
-  const uint32_t nact = min(static_cast<uint32_t>(U), (s.hi - min(s.hi, b0) + 31) >> 5);
+  // (measured, rejected: skipping the chunks no lane needs -- a warp-uniform count guarding
+  //  each chunk's load, gather and add -- C2 kernel 2.76 vs 2.63 ms, C4 7.55 vs 6.68: the
+  //  guarded chunks no longer batch their LDS gathers ahead of the arithmetic)
 #pragma unroll
   for (int u = 0; u < U; ++u) {
-    if (static_cast<uint32_t>(u) < nact) {
-      r[u] = M::filler(safe_col);
-      if (mask & (1u << u)) r[u] = mat.load(base + 32 * u);
-    }
+    r[u] = M::filler(safe_col);
+    if (mask & (1u << u)) r[u] = mat.load(base + 32 * u);
   }
   return mask;
 }
@@ -280,26 +279,6 @@ __device__ __forceinline__ void consume_batch(const typename M::Raw* r, uint32_t
         const Acc p = Ops::prod(M::v_of(r[g + u]), xv[u]);
         acc = Ops::add(acc, (mask & (1u << (g + u))) ? p : Acc(0));
       }
-    }
-  }
-}
-
-// Edge batch (some lane's mask is not full; called by the whole warp): only the chunks some lane
-// still needs -- the warp-uniform count
-// nact = 1 + the highest chunk any lane has -- are gathered and accumulated; the rest of the
-// batch (on average ~3.5 of 8 chunks at a segment's end) costs no LDS and no arithmetic.
-// Adding a masked product's +0.0 or skipping it leaves the accumulator's bits unchanged.
-template <int U, class M, typename Acc, class X>
-__device__ __forceinline__ void consume_edge(const typename M::Raw* r, uint32_t mask, const X& xr,
-                                             Acc& acc) {
-  using Ops = AccOps<Acc>;
-  const uint32_t any = __reduce_or_sync(kFull, mask);
-  const uint32_t nact = 32u - __clz(any);
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    if (static_cast<uint32_t>(u) < nact) {
-      const Acc p = Ops::prod(M::v_of(r[u]), xr(M::c_of(r[u])));
-      acc = Ops::add(acc, (mask & (1u << u)) ? p : Acc(0));
     }
   }
 }
@@ -346,15 +325,8 @@ __device__ __forceinline__ void run_segments(const M& mat, const XWindow<Acc>& x
         prefetch_batches<U, P + 1>(mat, seg_run<U>(sn), 0, lane);
       }
     }
-    // warp-uniform choice (lanes of an edge batch may hold a full mask of their own)
-    if (!__all_sync(kFull, mc == kFullMask<U>)) {
-      if (cur.flags & kSegGlobalX) consume_edge<U, M>(rc, mc, xg, acc);
-      else consume_edge<U, M>(rc, mc, xw, acc);
-    } else if (cur.flags & kSegGlobalX) {
-      consume_batch<U, M>(rc, mc, xg, acc);
-    } else {
-      consume_batch<U, M>(rc, mc, xw, acc);
-    }
+    if (cur.flags & kSegGlobalX) consume_batch<U, M>(rc, mc, xg, acc);
+    else consume_batch<U, M>(rc, mc, xw, acc);
     if (more) {
       ++bi;
       return true;
@@ -441,8 +413,7 @@ __global__ void __launch_bounds__(256)
       nx_pf = true;
       prefetch_batches<U, P + 1>(mat, nxt, 0, lane);
     }
-    if (!__all_sync(kFull, mc == kFullMask<U>)) consume_edge<U, M>(rc, mc, xg, acc);
-    else consume_batch<U, M>(rc, mc, xg, acc);
+    consume_batch<U, M>(rc, mc, xg, acc);
     if (more) {
       ++bi;
       return true;

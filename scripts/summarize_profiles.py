@@ -17,7 +17,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
-PROF = os.path.join(ROOT, "profiles")
+PROF = os.environ.get("DG_PROFILES_OUT", os.path.join(ROOT, "profiles"))
 sys.path.insert(0, os.path.join(ROOT, "scripts"))
 
 
@@ -82,8 +82,16 @@ def ncu(tag, family):
         u = units[hdr.index(k)]
         return v * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}.get(u, 1)
 
-    # one dose's kernels (k_tiles, and k_dense when it ran beside it): their bytes add up
-    return sum(get(v, "dram__bytes_read.sum") + get(v, "dram__bytes_write.sum") for v in r[2:])
+    # one dose's kernels (k_tiles, and k_dense when the plan uses it): the first capture of each
+    # kernel, bytes added up
+    seen, tot = set(), 0.0
+    for v in r[2:]:
+        name = v[hdr.index("Kernel Name")].split("<")[0] if "Kernel Name" in hdr else ""
+        if name in seen:
+            continue
+        seen.add(name)
+        tot += get(v, "dram__bytes_read.sum") + get(v, "dram__bytes_write.sum")
+    return tot
 
 
 def main():
@@ -94,7 +102,7 @@ def main():
     tf = os.path.join(PROF, "dram_bytes_per_launch.json")
     traffic = json.load(open(tf)) if os.path.exists(tf) else {}
     # keys: <config>:<accumulation>:<kernel name in dg_kernel_times> (read by bench.py)
-    for fam, key in (("exact", "c2:exact:tiles[w0]+dense"), ("fp32", "c2:fp32:tiles[w0]+dense"),
+    for fam, key in (("exact", "c2:exact:tiles[w0]"), ("fp32", "c2:fp32:tiles[w0]"),
                      ("c4", "c4:exact:tiles[fused]")):
         t = ncu(tag, fam)
         if t is not None:
