@@ -397,6 +397,9 @@ int run_kernels(Handle* h, const double* d_x, double* d_y, cudaStream_t s) {
 }
 
 int finish_create(Handle* h, const std::vector<uint64_t>& lens) {
+  // row ids in the plan (bins, segments, dense list) are u32: one handle holds < 2^32 rows
+  // (a larger matrix is row-sharded over several handles, dg_options.row_begin / row_end)
+  if (h->rows > 0xFFFFFFFFull) return DG_ERR_UNSUPPORTED_FEATURE;
   DG_CUDA(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device));
   const char* plan = std::getenv("DG_PLAN");  // "warp": v0 warp-per-row plan (A/B only)
   h->use_tiles = h->lane_width == 32 && !(plan && std::strcmp(plan, "warp") == 0);
