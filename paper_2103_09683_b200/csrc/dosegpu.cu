@@ -190,14 +190,17 @@ int launch_tiles_cfg(Handle* h, const M& mat, const Acc* x, double* y, cudaStrea
                                  static_cast<int>(smem)));
     h->tiles_attr = true;
   }
-  DG_CUDA(cudaMemsetAsync(h->d_counters, 0, Handle::kMaxWaves * sizeof(uint32_t), s));
+  // (after k_dense with programmatic launch, the counters were reset before k_dense: the tile
+  //  kernel must be the next operation in the stream)
+  if (!h->pdl_next) DG_CUDA(cudaMemsetAsync(h->d_counters, 0, Handle::kMaxWaves * sizeof(uint32_t), s));
   BlockSignal sig{nullptr, nullptr, 0};
   if (h->signal_blocks) {
     DG_CUDA(cudaMemcpyAsync(h->d_blk_left, h->d_blk_left_init, h->n_blocks * sizeof(uint32_t),
                             cudaMemcpyDeviceToDevice, s));
     sig = {h->d_blk_left, h->d_blk_flag, h->epoch};
   }
-  DG_CUDA(cudaEventRecord(h->ev_tiles_start, s));  // every row not owned by a tile is final here
+  if (h->signal_blocks)  // every row not owned by a tile is final here
+    DG_CUDA(cudaEventRecord(h->ev_tiles_start, s));
   static const char* const kWaveName[] = {"tiles[w0]", "tiles[w1]", "tiles[w2]", "tiles[w3]",
                                           "tiles[w4]", "tiles[w5]", "tiles[w6]", "tiles[w7]",
                                           "tiles[w8+]"};
@@ -211,10 +214,23 @@ int launch_tiles_cfg(Handle* h, const M& mat, const Acc* x, double* y, cudaStrea
   for (uint32_t w = 0; w < h->n_waves; ++w) {
     if (!h->wave_tiles[w]) continue;
     const int grid = std::min<int>(h->sm_count, static_cast<int>(h->wave_tiles[w]));
-    k_tiles<M, Acc, kWarps, kU, kR, kP, kNB, kCarry><<<grid, kWarps * 32, smem, s>>>(
-        mat, x, static_cast<const Tile*>(h->d_tiles[w]), h->wave_tiles[w],
-        static_cast<const Segment*>(h->d_segs[w]), carry, y, h->d_counters + w, h->window_cols,
-        sig, h->gt, w == 0 ? tr : TileTrace{nullptr, nullptr});
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(kWarps * 32);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    if (h->pdl_next && w == 0) {  // overlaps the tail of k_dense (launched just before)
+      lc.attrs = at;
+      lc.numAttrs = 1;
+    }
+    DG_CUDA(cudaLaunchKernelEx(&lc, k_tiles<M, Acc, kWarps, kU, kR, kP, kNB, kCarry>, mat, x,
+                               static_cast<const Tile*>(h->d_tiles[w]), h->wave_tiles[w],
+                               static_cast<const Segment*>(h->d_segs[w]), carry, y,
+                               h->d_counters + w, h->window_cols, sig, h->gt,
+                               w == 0 ? tr : TileTrace{nullptr, nullptr}));
     if (h->fused_waves)
       h->post(s, "tiles[fused]", h->fused_rows, h->fused_nnz);
     else
@@ -246,9 +262,17 @@ TileCfg tile_cfg_of(int cfg, bool packed) {
 // owns is final before the tile kernel -- and the row-block completion signals -- start.
 template <class M, typename Acc>
 int launch_dense(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t s) {
+  h->pdl_next = false;
   if (!h->n_dense_rows) return DG_OK;
   DG_CUDA(cudaMemsetAsync(h->d_dense_counter, 0, sizeof(uint32_t), s));
-  const int grid = grid_for(h->n_dense_rows * 32ull, 256, 8);
+  // The tile kernel follows as a programmatic dependent launch (it may start on SMs k_dense has
+  // left while k_dense's last rows finish) unless something must sit between the two launches:
+  // per-launch profiling events, or the row-block signals of the overlapped host download.
+  h->pdl_next = h->pdl && h->n_waves && !h->profiling && !h->signal_blocks && !h->d_trace;
+  if (h->pdl_next)
+    DG_CUDA(cudaMemsetAsync(h->d_counters, 0, Handle::kMaxWaves * sizeof(uint32_t), s));
+  // persistent when followed programmatically: every CTA resident (and triggered) at once
+  const int grid = h->pdl_next ? h->sm_count * 4 : grid_for(h->n_dense_rows * 32ull, 256, 8);
   switch (h->dense_cfg) {
     case 1:
       k_dense<M, Acc, 16, 2><<<grid, 256, 0, s>>>(mat, h->d_row_ptr, x, h->d_dense_rows,
@@ -415,6 +439,7 @@ int finish_create(Handle* h, const std::vector<uint64_t>& lens) {
   if (const char* dk = std::getenv("DG_DENSE")) h->dense_mode = std::atoi(dk) != 0;
   if (const char* dm = std::getenv("DG_DENSE_MIN_LEN")) h->dense_min_len = std::strtoull(dm, nullptr, 10);
   if (const char* dc = std::getenv("DG_DENSE_CFG")) h->dense_cfg = std::atoi(dc);
+  if (const char* pd = std::getenv("DG_PDL")) h->pdl = std::atoi(pd) != 0;
   if (const char* gm = std::getenv("DG_GLOBAL_MIN_LEN"))
     h->global_min_len = std::strtoull(gm, nullptr, 10);
   h->window_cols = window_bytes_for(h->tile_cfg, h->packed) / h->acc_bytes;

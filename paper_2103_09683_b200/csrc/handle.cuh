@@ -61,6 +61,8 @@ struct Handle {
   uint32_t* d_dense_counter = nullptr;
   uint64_t n_dense_rows = 0, dense_nnz = 0;
   int dense_cfg = 0;  // DG_DENSE_CFG: (U, P) = (8, 4) default, 1: (16, 2), 2: (8, 8)
+  bool pdl = true;       // DG_PDL: tile kernel as a programmatic dependent launch after k_dense
+  bool pdl_next = false; // (this dose: the next launch is that dependent launch)
   uint32_t wave_tiles[kMaxWaves] = {};
   uint64_t wave_nnz[kMaxWaves] = {}, wave_rows[kMaxWaves] = {};
   void* d_tiles[kMaxWaves] = {};

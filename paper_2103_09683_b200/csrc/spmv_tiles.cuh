@@ -375,6 +375,10 @@ __global__ void __launch_bounds__(256)
             double* __restrict__ y, GatherTargets gt) {
   using Ops = AccOps<Acc>;
   using Raw = typename M::Raw;
+  // programmatic dependent launch: the tile kernel that follows may take each SM as soon as
+  // this grid's CTAs there have exited (it touches other rows; it waits for this grid only
+  // before it completes)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const uint32_t lane = threadIdx.x & 31;
   const XGlobal<Acc> xg{x};
   auto grab = [&](SegRun& r) -> bool {
@@ -696,6 +700,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     __syncwarp();
     b = b + 1 == NB ? 0 : b + 1;
   }
+  // launched programmatically after k_dense: complete only after it (and its d rows)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (tr.cta && lane == 0) {
     atomicAdd(&tr.cta[4ull * blockIdx.x + 2], static_cast<unsigned long long>(wait_cyc));
     atomicAdd(&tr.cta[4ull * blockIdx.x + 3], static_cast<unsigned long long>(clock64() - clk0));
