@@ -44,13 +44,14 @@ constexpr uint32_t kSegWaveShift = 8;  // flags >> 8: the segment's index within
 // slot - 1.  Slots hold kCarryEmpty (a signalling NaN: arithmetic never produces one, every
 // partial is a quieted sum) until written, and the reader puts kCarryEmpty back for the next
 // dose, so a lane's partial is its own readiness flag: lane l of segment k + 1 spins only on its
-// own 8 bytes (one naturally aligned store / load: never torn), with no acquire/release pair
-// and no warp-wide flag.  That lets the warp `peek` the
-// next segment's carried partials when it grabs that segment (one segment ahead) and find them
-// already in registers at the switch.  The same code serves one launch per wave and all waves in
-// one launch (fused): in a persistent grid the wait is deadlock-free because tiles are claimed
-// wave after wave and a warp takes its segments in claim order, so a waiting segment only ever
-// waits on a lower wave's segment that is already claimed by a running warp.
+// own 8 bytes (one naturally aligned store / load: never torn), with no acquire/release pair and
+// no warp-wide flag.  That lets the warp `peek` the next segment's carried partials when it
+// grabs that segment (one segment ahead) and find them already in registers at the switch.
+// The same code serves one launch per wave and all waves in one launch (fused).  Fused, the
+// wait is deadlock-free in a persistent grid: the plan lists a row's segment k before its
+// segment k + 1 (plan.cu), tiles are claimed in list order and a warp takes its segments in
+// claim order, so a waiting segment only waits on an earlier-listed segment, and the earliest
+// unfinished segment never waits.
 template <typename Acc>
 struct CarryBits;
 template <>
