@@ -510,3 +510,70 @@ def test_overlapped_download_matches_device_result(monkeypatch):
     monkeypatch.setenv("DG_NO_OVERLAP", "1")
     with dg.DoseEngine.generate(p) as e:
         assert np.array_equal(bits(e.dose(x)), bits(yh))
+
+
+def _edge_values(rng, n):
+    """binary16 bit patterns: both signs, subnormals, normals up to the largest finite."""
+    v = rng.choice([0x0001, 0x03FF, 0x0400, 0x3C00, 0x7BFF, 0x8001, 0xBC00, 0xFBFF], n)
+    mix = rng.random(n) < 0.7
+    v[mix] = (rng.random(mix.sum()) * 2 - 1).astype(np.float16).view(np.uint16)[:mix.sum()]
+    return v.astype(np.uint16)
+
+
+@pytest.mark.parametrize("dense", ["0", "1"])
+def test_edge_max_u16_width_and_special_values(port, monkeypatch, dense):
+    """cols = 65535 (the widest U16 matrix): a fully dense 65535-long row (k_dense or global-x
+    tiles), rows touching columns 0 and 65534, sparse rows over the whole width (split into
+    waves), value bits with both signs / subnormals / the largest finite half, and an x with
+    negatives, subnormals, -0.0 and magnitudes up to 1e290 (no sum overflows: an Inf - Inf NaN's
+    payload is platform-defined)."""
+    monkeypatch.setenv("DG_DENSE", dense)
+    rng = np.random.default_rng(11)
+    cols = 65_535
+    rows_cols = [np.arange(cols), np.array([0, cols - 1]), np.array([cols - 1]), np.array([0])]
+    for _ in range(200):
+        n = int(rng.integers(1, 5000))
+        rows_cols.append(np.sort(rng.choice(cols, n, replace=False)))
+    for _ in range(100):
+        rows_cols.append(np.array([], dtype=np.int64))
+    rng.shuffle(rows_cols)
+    lens = np.array([len(c) for c in rows_cols])
+    rp = np.zeros(len(rows_cols) + 1, dtype=np.uint64)
+    np.cumsum(lens, out=rp[1:])
+    col = np.concatenate(rows_cols).astype(np.uint32)
+    m = Csr(len(rows_cols), cols, HALF, U16, rp, col, _edge_values(rng, len(col)))
+    x = rng.standard_normal(cols) * np.exp(rng.uniform(-700, 668, cols))  # no sum overflows
+    x[rng.choice(cols, 50, replace=False)] = -0.0
+    x[rng.choice(cols, 50, replace=False)] = 5e-324
+    want = port.spmv_rowchunk(m, x, 32, 2)
+    with dg.DoseEngine.from_csr(to_dg(m)) as e:
+        assert np.array_equal(bits(e.dose(x)), bits(want))
+
+
+def test_edge_odd_cols_unaligned_x(port):
+    """cols not a multiple of 2 (x rows are staged into the padded buffer for TMA) and x passed
+    from an unaligned device address."""
+    import torch
+    rng = np.random.default_rng(4)
+    cols = 4095
+    entries = [(r, int(c), float(rng.random()))
+               for r in range(600) for c in rng.choice(cols, int(rng.integers(0, 300)), replace=False)]
+    m = make_csr(600, cols, entries, HALF, port, U16)
+    x = port.seeded_vector(cols, 42)
+    want = bits(port.spmv_rowchunk(m, x, 32, 2))
+    with dg.DoseEngine.from_csr(to_dg(m)) as e:
+        assert np.array_equal(bits(e.dose(x)), want)
+        buf = torch.zeros(cols + 1, dtype=torch.float64, device="cuda")
+        buf[1:] = torch.from_numpy(x).cuda()
+        y = torch.empty(600, dtype=torch.float64, device="cuda")
+        e.dose_device(buf[1:].data_ptr(), cols, y.data_ptr())  # 8-byte, not 16-byte aligned
+        assert np.array_equal(y.cpu().numpy().view(np.uint64), want)
+
+
+def test_edge_no_rows_no_nonzeros(port):
+    """rows = 0, and rows > 0 with nnz = 0 (every row empty: +0.0)."""
+    m0 = make_csr(0, 3, [], HALF, port, U16)
+    assert len(dg.spmv_rowchunk(to_dg(m0), np.ones(3))) == 0
+    m1 = make_csr(5, 7, [], HALF, port, U16)
+    y = dg.spmv_rowchunk(to_dg(m1), np.arange(7, dtype=np.float64))
+    assert len(y) == 5 and np.all(bits(y) == 0)
