@@ -310,11 +310,17 @@ int launch_tiles(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t 
       case 11: return launch_tiles_cfg<M, Acc, 32, 8, 0, 0>(h, mat, x, y, s);
       case 12: return launch_tiles_cfg<M, Acc, 32, 8, 0, kP, 3>(h, mat, x, y, s);
       case 13: return launch_tiles_cfg<M, Acc, 32, 8, 0, kP, 4>(h, mat, x, y, s);
+      // (A/B: narrow batches with P = 4; U = 4, P = 2 is the short-segment default below)
+      case 19: return launch_tiles_cfg<M, Acc, 32, 4, 0, 4>(h, mat, x, y, s);
       // (measured, rejected: wider batches U = 12 at 32 / 28 warps, U = 16 at 28 warps --
       //  C2 2.70 / 2.66 / 2.82 ms vs 2.62; profiles/README.md)
       // (measured, rejected: cp.async.bulk.prefetch.L2 by one lane instead of per-line
       //  prefetches, P = 2/4/8 -- C2 2.94-3.00 ms vs 2.80; profiles/README.md)
       default:
+        // short segments (mean < 256 nonzeros, C1: 136): 4-chunk batches waste fewer masked
+        // chunks at each segment's end (C1 0.157 -> 0.148 ms; C2 would lose: 2.63 -> 3.19)
+        if (!h->n_carry_slots && h->short_segments)
+          return launch_tiles_cfg<M, Acc, Handle::kTileWarps, 4, 0, 2, 2, false>(h, mat, x, y, s);
         if (!h->n_carry_slots)  // no split rows: the carry code is compiled out
           return launch_tiles_cfg<M, Acc, Handle::kTileWarps, Handle::kTileUnroll, 0, kP, 2, false>(
               h, mat, x, y, s);

@@ -69,6 +69,7 @@ struct Handle {
   void* d_segs[kMaxWaves] = {};
   void* d_state = nullptr;
   bool fused_waves = false;            // all waves in one launch (wave 0's list)
+  bool short_segments = false;         // mean tile segment < 256 nonzeros: 4-chunk batches
   uint64_t n_carry_slots = 0;          // split-row boundaries (32 partials each, Carry)
   uint64_t fused_rows = 0, fused_nnz = 0;
   uint32_t* d_counters = nullptr;

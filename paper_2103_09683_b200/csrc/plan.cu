@@ -380,6 +380,15 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     }
     if (blk != kNoBlock) h->blk_tiles[k] += static_cast<uint32_t>(tiles.size() - tiles_before);
   }
+  {
+    uint64_t nseg = 0, snnz = 0;
+    for (uint32_t lw = 0; lw < NL; ++lw) {
+      nseg += lsegs[lw].size();
+      snnz += ldone[lw];
+    }
+    h->short_segments = nseg && snnz < 256ull * nseg;
+    if (const char* ss = std::getenv("DG_SHORT_SEGMENTS")) h->short_segments = std::atoi(ss) != 0;
+  }
   for (uint32_t w = 0; w < NW; ++w) {
     h->wave_nnz[w] = wnnz[w];
     h->wave_rows[w] = wrows[w];

@@ -577,3 +577,19 @@ def test_edge_no_rows_no_nonzeros(port):
     m1 = make_csr(5, 7, [], HALF, port, U16)
     y = dg.spmv_rowchunk(to_dg(m1), np.arange(7, dtype=np.float64))
     assert len(y) == 5 and np.all(bits(y) == 0)
+
+
+@pytest.mark.parametrize("short", ["0", "1"])
+def test_batch_width_both_paths_desk(port, golden, desk, monkeypatch, short):
+    """4-chunk batches (short segments, chosen automatically when the mean segment is < 256
+    nonzeros) and 8-chunk batches give the reference's bits on both desk profiles and C1-like
+    rows."""
+    monkeypatch.setenv("DG_SHORT_SEGMENTS", short)
+    for name in ("liver-desk", "prostate-desk"):
+        m = desk[name]
+        x = port.seeded_vector(m.cols, 42)
+        y = dg.spmv_rowchunk(to_dg(m), x)
+        assert f"{dg.checksum_bits(y):016x}" == golden[name]["rowchunk"]["32"], name
+    m = _wide_row_matrix(port, rows=2000, split=False)
+    x = port.seeded_vector(m.cols, 42)
+    assert np.array_equal(bits(dg.spmv_rowchunk(to_dg(m), x)), bits(port.spmv_rowchunk(m, x, 32, 2)))
