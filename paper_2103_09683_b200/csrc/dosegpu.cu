@@ -335,6 +335,7 @@ int launch_tiles(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t 
   // vs 6.80 at 24 warps without the peek, 7.37 at 16 warps)
   switch (h->tile_cfg) {
     case 30: return launch_tiles_cfg<M, Acc, 24, Handle::kTileUnroll, 0, kP>(h, mat, x, y, s);
+    // (measured, rejected: 4-chunk batches at 24 / 32 warps -- C4 7.49 / 7.12 ms vs 6.65)
     default: return launch_tiles_cfg<M, Acc, 20, Handle::kTileUnroll, 0, kP>(h, mat, x, y, s);
   }
 }
