@@ -26,7 +26,16 @@
 #include "common.cuh"
 #include "spmv_kernels.cuh"
 
+// DG_ROTATE=1: rotated lane grid (aligned chunk loads).  Bit-identical, measured: C2 kernel
+// 2.634 vs 2.633 ms, C1 0.156 vs 0.141, C4 6.69 vs 6.65 (every row's first batch becomes an
+// edge batch) -- off.
+#ifndef DG_ROTATE
+#define DG_ROTATE 0
+#endif
+
 namespace dg {
+
+constexpr bool kRotate = DG_ROTATE;  // rotated lane grid (SegRun) in k_tiles and k_dense
 
 struct Segment {  // 24 bytes
   uint64_t p0;     // first position (shard-local nnz index)
@@ -191,21 +200,47 @@ struct XGlobal {
 // A segment as the warp's pipeline sees it: batches of U chunks of 32 positions aligned to the
 // row's lane grid (chunk c covers base0 + 32c + lane); positions outside [p0, p1) are masked.
 struct SegRun {
-  uint64_t base0;   // row-aligned start: positions base0 + rel, rel in [lo, hi) are the segment's
-  uint32_t lo, hi;  // lo = lane0, hi = lane0 + n
+  uint64_t base0;   // chunk grid start: positions base0 + rel, rel in [lo, hi) are the segment's
+  uint32_t lo, hi;  // (unrotated: base0 = the row's lane grid, lo = lane0, hi = lane0 + n)
   uint32_t nbatch, row, slot, flags;
+  uint32_t rot;     // rotated grid: physical lane p holds the row's logical lane (p - rot) & 31
 };
-template <int U>
-__device__ __forceinline__ SegRun seg_run(const Segment& S) {
+// Rotated lane grid (ROT): chunks start on 128-byte boundaries of the stream (base0 rounded down
+// to a multiple of 32 positions), so every chunk load is one aligned line instead of straddling
+// two.  Physical lane p then holds the row's logical lane (p - rot) & 31 with rot = row_start &
+// 31 -- the same for every segment of a row, so carried partials stay lane-consistent -- and
+// still sees that lane's positions in increasing order; positions before the row are masked
+// like any edge; the final tree shuffles by (lane + w) & 31 and lane rot holds the result.
+template <int U, bool ROT = false>
+__device__ __forceinline__ SegRun seg_run_at(uint64_t base0, uint32_t lo, uint32_t n) {
   SegRun r;
-  r.base0 = S.p0 - S.lane0;
-  r.lo = S.lane0;
-  r.hi = S.lane0 + S.n;
+  const uint32_t rot = ROT ? static_cast<uint32_t>(base0 & 31u) : 0u;
+  r.base0 = base0 - rot;
+  r.lo = lo + rot;
+  r.hi = lo + n + rot;
+  r.rot = rot;
   r.nbatch = ((r.hi + 31) / 32 + U - 1) / U;
+  return r;
+}
+template <int U, bool ROT = false>
+__device__ __forceinline__ SegRun seg_run(const Segment& S) {
+  SegRun r = seg_run_at<U, ROT>(S.p0 - S.lane0, S.lane0, S.n);
   r.row = S.row;
   r.slot = S.slot;
   r.flags = S.flags;
   return r;
+}
+// The reference's stride-halving tree (src/spmv.cpp:64-65) over the 32 logical lanes; returns
+// true on the lane that holds the row's result.
+template <bool ROT, typename Acc>
+__device__ __forceinline__ bool row_tree(Acc& acc, uint32_t lane, uint32_t rot) {
+  using Ops = AccOps<Acc>;
+#pragma unroll
+  for (int off = 16; off >= 1; off /= 2) {
+    if constexpr (ROT) acc = Ops::add(acc, __shfl_sync(kFull, acc, (lane + off) & 31u));
+    else acc = Ops::add(acc, __shfl_down_sync(kFull, acc, off));
+  }
+  return lane == (ROT ? rot : 0u);
 }
 
 // Issue batch b of segment s: U predicated requests (one 128-B request per chunk for Packed16).
@@ -300,7 +335,7 @@ __device__ __forceinline__ void run_segments(const M& mat, const XWindow<Acc>& x
   using Raw = typename M::Raw;
   Segment sd;
   if (!grab(sd)) return;
-  SegRun cur = seg_run<U>(sd);
+  SegRun cur = seg_run<U, kRotate>(sd);
   Segment sn;
   bool have_next = grab(sn);
   Acc carried_next = PEEK && have_next ? carry.peek(sn.slot, sn.flags, lane) : Acc(0);
@@ -315,7 +350,7 @@ __device__ __forceinline__ void run_segments(const M& mat, const XWindow<Acc>& x
   auto step = [&](const Raw* rc, uint32_t mc, Raw* rn, uint32_t& mn) -> bool {
     const bool more = bi + 1 < cur.nbatch;
     if (more) mn = load_batch<U>(mat, rn, cur, bi + 1, lane, safe);
-    else if (have_next) mn = load_batch<U>(mat, rn, seg_run<U>(sn), 0, lane, safe);
+    else if (have_next) mn = load_batch<U>(mat, rn, seg_run<U, kRotate>(sn), 0, lane, safe);
     if constexpr (P > 0) {  // the L2 prefetch stream runs P batches ahead of the loads; once
       // it passes the end of this segment, the next segment's first P + 1 batches go at once
       const uint32_t pf = bi + 1 + P;
@@ -323,7 +358,7 @@ __device__ __forceinline__ void run_segments(const M& mat, const XWindow<Acc>& x
         prefetch_batches<U, 1>(mat, cur, pf, lane);
       } else if (have_next && !sn_pf) {
         sn_pf = true;
-        prefetch_batches<U, P + 1>(mat, seg_run<U>(sn), 0, lane);
+        prefetch_batches<U, P + 1>(mat, seg_run<U, kRotate>(sn), 0, lane);
       }
     }
     if (cur.flags & kSegGlobalX) consume_batch<U, M>(rc, mc, xg, acc);
@@ -333,9 +368,7 @@ __device__ __forceinline__ void run_segments(const M& mat, const XWindow<Acc>& x
       return true;
     }
     if (!CARRY || (cur.flags & kSegLast)) {
-#pragma unroll
-      for (int off = 16; off >= 1; off /= 2) acc = Ops::add(acc, __shfl_down_sync(kFull, acc, off));
-      if (lane == 0) {
+      if (row_tree<kRotate>(acc, lane, cur.rot)) {
         y[cur.row] = static_cast<double>(acc);
         gt.store(cur.row, static_cast<double>(acc));
       }
@@ -343,7 +376,7 @@ __device__ __forceinline__ void run_segments(const M& mat, const XWindow<Acc>& x
       if constexpr (CARRY) carry.out(cur.slot, cur.flags, lane, acc);
     }
     if (!have_next) return false;
-    cur = seg_run<U>(sn);
+    cur = seg_run<U, kRotate>(sn);
     bi = 0;
     if constexpr (PEEK) acc = carry.take(cur.slot, cur.flags, lane, carried_next);
     else acc = CARRY ? carry.in(cur.slot, cur.flags, lane) : Acc(0);
@@ -389,10 +422,7 @@ __global__ void __launch_bounds__(256)
     if (k >= n_rows) return false;
     const uint32_t row = rows[k];
     const uint64_t s = rp[row], e = rp[row + 1];
-    r.base0 = s;
-    r.lo = 0;
-    r.hi = static_cast<uint32_t>(e - s);
-    r.nbatch = ((r.hi + 31) / 32 + U - 1) / U;
+    r = seg_run_at<U, kRotate>(s, 0u, static_cast<uint32_t>(e - s));
     r.row = row;
     r.slot = 0;
     r.flags = kSegFirst | kSegLast;
@@ -423,9 +453,7 @@ __global__ void __launch_bounds__(256)
       ++bi;
       return true;
     }
-#pragma unroll
-    for (int off = 16; off >= 1; off /= 2) acc = Ops::add(acc, __shfl_down_sync(kFull, acc, off));
-    if (lane == 0) {
+    if (row_tree<kRotate>(acc, lane, cur.rot)) {
       y[cur.row] = static_cast<double>(acc);
       gt.store(cur.row, static_cast<double>(acc));
     }
