@@ -336,6 +336,7 @@ int launch_tiles(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t 
   switch (h->tile_cfg) {
     case 30: return launch_tiles_cfg<M, Acc, 24, Handle::kTileUnroll, 0, kP>(h, mat, x, y, s);
     // (measured, rejected: 4-chunk batches at 24 / 32 warps -- C4 7.49 / 7.12 ms vs 6.65)
+    // (measured, rejected: 18 / 22 warps -- C4 7.02 / 6.88 ms vs 6.65 at 20)
     default: return launch_tiles_cfg<M, Acc, 20, Handle::kTileUnroll, 0, kP>(h, mat, x, y, s);
   }
 }
