@@ -102,13 +102,19 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
   //    reads x from global (its lanes read consecutive x: 2 sectors per 32 positions); a sparse
   //    wide row (e.g. a multi-beam row of C4) is cut greedily into windowed segments, one wave
   //    per segment, carrying its 32 lane partials between waves
-  // k_dense on/off (DG_DENSE=0/1 forces it): on when the longest dense row is a sizeable share of
-  // one SM's work (nnz < 200 * SMs * longest) -- there a warp streaming such a row inside the tile
-  // kernel sets the kernel tail (C2's 1/8 shard: 0.466 -> 0.415 ms); off on large matrices, where
-  // the tile kernel absorbs long rows and k_dense only delays the overlapped d download
-  // (C2: step equal, end to end 2.96 -> 3.03 ms).
+  // k_dense for every dense row >= dense_min_len (DG_DENSE=0/1 forces off / on): when the longest
+  // dense row is a sizeable share of one SM's work (nnz < 200 * SMs * longest) -- there a warp
+  // streaming such a row inside the tile kernel sets the kernel tail (C2's 1/8 shard: 0.466 ->
+  // 0.415 ms); on large matrices windowed dense rows stay in the tiles (C2: moving them is neutral
+  // for the step and delays the overlapped d download).
   // It also needs the dense rows to be >= 5% of the nonzeros: a handful of long rows (C1 has one
   // or two) cost the tile kernel little and a separate launch more.
+  // Auto: dense rows wider than a window go to k_dense when they hold >= 1% of the nonzeros
+  // (inside the tile kernel they read x through L1 lines from L2: C2, 13% of the nonzeros,
+  // 2.76 -> 2.62 ms, end to end 2.79 -> 2.66; C4's few such rows would only add a launch), and
+  // every dense row >= dense_min_len does when the rule above holds (C3 shards).
+  bool dense_all = h->dense_mode > 0;
+  uint64_t wide_dense = 0;
   if (h->dense_mode < 0) {
     uint64_t longest = 0, dnnz = 0;
     for (uint64_t r = 0; r < rows; ++r) {
@@ -117,12 +123,12 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
       if (4 * lens[r] >= 3 * span) {
         longest = std::max<uint64_t>(longest, lens[r]);
         dnnz += lens[r];
+        if (span > ws) wide_dense += lens[r];
       }
     }
-    h->dense_kernel = longest && h->nnz < 200ull * h->sm_count * longest && 20 * dnnz >= h->nnz;
-  } else {
-    h->dense_kernel = h->dense_mode != 0;
+    dense_all = longest && h->nnz < 200ull * h->sm_count * longest && 20 * dnnz >= h->nnz;
   }
+  h->dense_kernel = h->dense_mode != 0 && (dense_all || 100 * wide_dense >= h->nnz);
   std::vector<std::vector<HostSeg>> waves(1);
   std::vector<HostSeg> global_x;
   std::vector<uint32_t> wide, dense_rows;
@@ -132,7 +138,8 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     const uint64_t span = static_cast<uint64_t>(c1) - c0 + 1;
     const uint16_t whole = static_cast<uint16_t>(kSegFirst | kSegLast);
     const bool dense = 4 * lens[r] >= 3 * span;
-    if (h->dense_kernel && dense && lens[r] >= h->dense_min_len) {  // k_dense
+    if (h->dense_kernel && dense && lens[r] >= h->dense_min_len &&
+        (dense_all || span > ws)) {  // k_dense
       dense_rows.push_back(static_cast<uint32_t>(r));
       h->dense_nnz += lens[r];
       continue;
