@@ -82,16 +82,15 @@ def ncu(tag, family):
         u = units[hdr.index(k)]
         return v * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}.get(u, 1)
 
-    # one dose's kernels (k_tiles, and k_dense when the plan uses it): the first capture of each
-    # kernel, bytes added up
-    seen, tot = set(), 0.0
+    # one dose's kernels (k_tiles, and k_dense when the plan uses it): DRAM bytes of the first
+    # capture of each kernel, keyed like bench.py's roofline.kernels names
+    out = {}
     for v in r[2:]:
-        name = v[hdr.index("Kernel Name")].split("<")[0] if "Kernel Name" in hdr else ""
-        if name in seen:
-            continue
-        seen.add(name)
-        tot += get(v, "dram__bytes_read.sum") + get(v, "dram__bytes_write.sum")
-    return tot
+        name = v[hdr.index("Kernel Name")] if "Kernel Name" in hdr else ""
+        key = "dense" if "k_dense" in name else "tiles"
+        if key not in out:
+            out[key] = get(v, "dram__bytes_read.sum") + get(v, "dram__bytes_write.sum")
+    return out
 
 
 def main():
@@ -102,12 +101,14 @@ def main():
     tf = os.path.join(PROF, "dram_bytes_per_launch.json")
     traffic = json.load(open(tf)) if os.path.exists(tf) else {}
     # keys: <config>:<accumulation>:<kernel name in dg_kernel_times> (read by bench.py)
-    for fam, key in (("exact", "c2:exact:tiles[w0]"), ("fp32", "c2:fp32:tiles[w0]"),
-                     ("c4", "c4:exact:tiles[fused]")):
+    for fam, prefix, tiles in (("exact", "c2:exact", "tiles[w0]"), ("fp32", "c2:fp32", "tiles[w0]"),
+                               ("c4", "c4:exact", "tiles[fused]")):
         t = ncu(tag, fam)
-        if t is not None:
-            traffic[key] = int(t)
-            print(fam, "dram bytes per launch", t)
+        if t is None:
+            continue
+        for k, b in t.items():
+            traffic[f"{prefix}:{tiles if k == 'tiles' else 'dense'}"] = int(b)
+            print(fam, k, "dram bytes per launch", b)
     json.dump(traffic, open(tf, "w"), indent=1, sort_keys=True)
 
 
