@@ -436,8 +436,9 @@ int finish_create(Handle* h, const std::vector<uint64_t>& lens) {
   const char* plan = std::getenv("DG_PLAN");  // "warp": v0 warp-per-row plan (A/B only)
   h->use_tiles = h->lane_width == 32 && !(plan && std::strcmp(plan, "warp") == 0);
   h->acc_bytes = h->accumulation == DG_ACCUM_FP32 ? 4 : 8;
-  // ~8 tiles per SM at least (small matrices), at most 1M nonzeros per tile (C2 sweep optimum)
-  h->tile_nnz = std::max<uint64_t>(16 * 1024, std::min<uint64_t>(1024 * 1024,
+  // ~8 tiles per SM at least (small matrices), at most 768K nonzeros per tile (C2 sweep: 512K-768K
+  // flat, 1M +0.6%, 1.5M +1%, with the rows wider than a window in k_dense; C4 / C5 flat)
+  h->tile_nnz = std::max<uint64_t>(16 * 1024, std::min<uint64_t>(768 * 1024,
                                                                   h->nnz / (8ull * h->sm_count)));
   if (const char* tn = std::getenv("DG_TILE_NNZ")) h->tile_nnz = std::strtoull(tn, nullptr, 10);
   if (const char* tc = std::getenv("DG_TILE_CFG")) h->tile_cfg = std::atoi(tc);
