@@ -110,6 +110,8 @@ struct GatherTargets {
   double* t[kMaxGatherTargets];
   uint32_t n;
   uint64_t row_off;
+  // kernels take it as `const __grid_constant__`: indexed in the parameter space directly (a
+  // by-value parameter indexed at run time was copied to the stack -- r01's 88-byte frame)
   __device__ __forceinline__ void store(uint64_t row, double v) const {
     for (uint32_t i = 0; i < n; ++i) t[i][row_off + row] = v;
   }

@@ -72,6 +72,17 @@ __global__ void k_unpack(M mat, uint64_t b, uint64_t n, uint32_t* __restrict__ c
   }
 }
 
+// x staging: dst0 <- src (skipped when they alias), dst1 (the shifted copy, XSource) <- src
+__global__ void k_stage_x(const double* __restrict__ src, double* dst0, double* __restrict__ dst1,
+                          uint64_t n) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const double v = src[i];
+    if (dst0 != src) dst0[i] = v;
+    if (dst1) dst1[i] = v;
+  }
+}
+
 __global__ void k_rebase(uint64_t* __restrict__ rp, uint64_t n, uint64_t base) {
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
@@ -179,13 +190,11 @@ void launch_group(Handle* h, int b, const char* name, cudaStream_t s, const M& m
 
 // One persistent launch per wave (one CTA per SM): wave k continues the segments whose lane
 // partials wave k-1 stored.
-template <class M, typename Acc, int kWarps, int kU, int kR = 0, int kP = 0, int kNB = 2,
-          bool kCarry = true>
+template <class M, typename Acc, int kWarps, int kU, int kP = 0, int kNB = 2, bool kCarry = true>
 int launch_tiles_cfg(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t s) {
-  const size_t smem = static_cast<size_t>(kNB) * h->window_cols * sizeof(Acc) +
-                      ring_smem_bytes<kWarps, kR>();
+  const size_t smem = static_cast<size_t>(kNB) * h->window_cols * sizeof(Acc);
   if (!h->tiles_attr) {  // a handle has one (M, Acc, config) and one device
-    DG_CUDA(cudaFuncSetAttribute(k_tiles<M, Acc, kWarps, kU, kR, kP, kNB, kCarry>,
+    DG_CUDA(cudaFuncSetAttribute(k_tiles<M, Acc, kWarps, kU, kP, kNB, kCarry>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
     h->tiles_attr = true;
@@ -226,7 +235,9 @@ int launch_tiles_cfg(Handle* h, const M& mat, const Acc* x, double* y, cudaStrea
       lc.attrs = at;
       lc.numAttrs = 1;
     }
-    DG_CUDA(cudaLaunchKernelEx(&lc, k_tiles<M, Acc, kWarps, kU, kR, kP, kNB, kCarry>, mat, x,
+    const XSource<Acc> xsrc{x, std::is_same_v<Acc, double> ? reinterpret_cast<const Acc*>(h->d_x1) : nullptr,
+                            h->rep_stride};
+    DG_CUDA(cudaLaunchKernelEx(&lc, k_tiles<M, Acc, kWarps, kU, kP, kNB, kCarry>, mat, xsrc,
                                static_cast<const Tile*>(h->d_tiles[w]), h->wave_tiles[w],
                                static_cast<const Segment*>(h->d_segs[w]), carry, y,
                                h->d_counters + w, h->window_cols, sig, h->gt,
@@ -240,21 +251,16 @@ int launch_tiles_cfg(Handle* h, const M& mat, const Acc* x, double* y, cudaStrea
   return DG_OK;
 }
 
-// Tile-kernel configurations (warps per CTA, batch depth U, TMA ring stages R, L2 prefetch
-// distance P, x-window buffers NB).  DG_TILE_CFG selects an alternative for measurement; the
-// default is the measured best on C2 (profiles/).  Config 6 is the TMA-ring variant of the matrix
-// stream (measured slower: instruction-bound), kept for A/B.
-struct TileCfg {
-  int nb;      // x-window buffers
-  bool ring;   // TMA-ring matrix stream (24 warps x 4 stages)
-};
-TileCfg tile_cfg_of(int cfg, bool packed) {
-  if (!packed) return {2, false};
+// Tile-kernel configurations (warps per CTA, batch depth U, L2 prefetch distance P, x-window
+// buffers NB).  DG_TILE_CFG selects an alternative for measurement; the default is the measured
+// best on C2 (profiles/).  (Rejected in r01 and removed: a per-warp TMA ring for the matrix
+// stream, 24 warps x 4 stages of 1 KB -- instruction-bound, C2 4.16 ms.)
+int tile_buffers_of(int cfg, bool packed) {
+  if (!packed) return 2;
   switch (cfg) {
-    case 6: return {2, true};
-    case 12: return {3, false};
-    case 13: return {4, false};
-    default: return {2, false};
+    case 12: return 3;
+    case 13: return 4;
+    default: return 2;
   }
 }
 
@@ -304,14 +310,13 @@ int launch_tiles(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t 
   constexpr int kP = std::is_same_v<Acc, float> ? 4 : 2;  // measured: prefetch distance
   if constexpr (std::is_same_v<M, Packed16>) {
     switch (h->tile_cfg) {
-      case 6: return launch_tiles_cfg<M, Acc, 24, 8, 4>(h, mat, x, y, s);
-      case 8: return launch_tiles_cfg<M, Acc, 32, 8, 0, 1>(h, mat, x, y, s);
-      case 10: return launch_tiles_cfg<M, Acc, 32, 8, 0, 4>(h, mat, x, y, s);
-      case 11: return launch_tiles_cfg<M, Acc, 32, 8, 0, 0>(h, mat, x, y, s);
-      case 12: return launch_tiles_cfg<M, Acc, 32, 8, 0, kP, 3>(h, mat, x, y, s);
-      case 13: return launch_tiles_cfg<M, Acc, 32, 8, 0, kP, 4>(h, mat, x, y, s);
+      case 8: return launch_tiles_cfg<M, Acc, 32, 8, 1>(h, mat, x, y, s);
+      case 10: return launch_tiles_cfg<M, Acc, 32, 8, 4>(h, mat, x, y, s);
+      case 11: return launch_tiles_cfg<M, Acc, 32, 8, 0>(h, mat, x, y, s);
+      case 12: return launch_tiles_cfg<M, Acc, 32, 8, kP, 3>(h, mat, x, y, s);
+      case 13: return launch_tiles_cfg<M, Acc, 32, 8, kP, 4>(h, mat, x, y, s);
       // (A/B: narrow batches with P = 4; U = 4, P = 2 is the short-segment default below)
-      case 19: return launch_tiles_cfg<M, Acc, 32, 4, 0, 4>(h, mat, x, y, s);
+      case 19: return launch_tiles_cfg<M, Acc, 32, 4, 4>(h, mat, x, y, s);
       // (measured, rejected: wider batches U = 12 at 32 / 28 warps, U = 16 at 28 warps --
       //  C2 2.70 / 2.66 / 2.82 ms vs 2.62; profiles/README.md)
       // (measured, rejected: cp.async.bulk.prefetch.L2 by one lane instead of per-line
@@ -320,35 +325,33 @@ int launch_tiles(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t 
         // short segments (mean < 256 nonzeros, C1: 136): 4-chunk batches waste fewer masked
         // chunks at each segment's end (C1 0.157 -> 0.148 ms; C2 would lose: 2.63 -> 3.19)
         if (!h->n_carry_slots && h->short_segments)
-          return launch_tiles_cfg<M, Acc, Handle::kTileWarps, 4, 0, 2, 2, false>(h, mat, x, y, s);
+          return launch_tiles_cfg<M, Acc, Handle::kTileWarps, 4, 2, 2, false>(h, mat, x, y, s);
         if (!h->n_carry_slots)  // no split rows: the carry code is compiled out
-          return launch_tiles_cfg<M, Acc, Handle::kTileWarps, Handle::kTileUnroll, 0, kP, 2, false>(
+          return launch_tiles_cfg<M, Acc, Handle::kTileWarps, Handle::kTileUnroll, kP, 2, false>(
               h, mat, x, y, s);
-        return launch_tiles_cfg<M, Acc, Handle::kTileWarps, Handle::kTileUnroll, 0, kP>(h, mat, x,
-                                                                                       y, s);
+        return launch_tiles_cfg<M, Acc, Handle::kTileWarps, Handle::kTileUnroll, kP>(h, mat, x, y, s);
     }
   }
   // SoA elements take two registers each: 24 warps leave room for two U = 8 batches
   if (!h->n_carry_slots)
-    return launch_tiles_cfg<M, Acc, 24, Handle::kTileUnroll, 0, kP, 2, false>(h, mat, x, y, s);
+    return launch_tiles_cfg<M, Acc, 24, Handle::kTileUnroll, kP, 2, false>(h, mat, x, y, s);
   // split rows: 20 warps leave 96 registers, room for the carried-partials peek (C4: 6.70 ms
   // vs 6.80 at 24 warps without the peek, 7.37 at 16 warps)
   switch (h->tile_cfg) {
-    case 30: return launch_tiles_cfg<M, Acc, 24, Handle::kTileUnroll, 0, kP>(h, mat, x, y, s);
+    case 30: return launch_tiles_cfg<M, Acc, 24, Handle::kTileUnroll, kP>(h, mat, x, y, s);
     // (measured, rejected: 4-chunk batches at 24 / 32 warps -- C4 7.49 / 7.12 ms vs 6.65)
     // (measured, rejected: 18 / 22 warps -- C4 7.02 / 6.88 ms vs 6.65 at 20)
-    default: return launch_tiles_cfg<M, Acc, 20, Handle::kTileUnroll, 0, kP>(h, mat, x, y, s);
+    default: return launch_tiles_cfg<M, Acc, 20, Handle::kTileUnroll, kP>(h, mat, x, y, s);
   }
 }
 
-// Bytes of one x-window buffer: what is left of the 227 KB of shared memory per CTA after the
-// TMA rings, split in NB buffers, rounded down to 1 KB.
+// Bytes of one x-window buffer: two buffers of kWindowBytes, or what is left of the 227 KB of
+// shared memory per CTA split in NB buffers, rounded down to 3 KB (whole replicas in slot mode).
 uint32_t window_bytes_for(int cfg, bool packed) {
   constexpr size_t kMaxDyn = 232448 - 256;  // cudaDevAttrMaxSharedMemoryPerBlockOptin - static
-  const TileCfg c = tile_cfg_of(cfg, packed);
-  const size_t ring = c.ring ? ring_smem_bytes<24, 4>() : 0;
-  if (!ring && c.nb == 2) return kWindowBytes;
-  return static_cast<uint32_t>(((kMaxDyn - ring) / c.nb) & ~size_t(1023));
+  const int nb = tile_buffers_of(cfg, packed);
+  if (nb == 2) return kWindowBytes;
+  return static_cast<uint32_t>(kMaxDyn / nb / 3072 * 3072);
 }
 
 template <class M>
@@ -452,15 +455,26 @@ int finish_create(Handle* h, const std::vector<uint64_t>& lens) {
   if (const char* gm = std::getenv("DG_GLOBAL_MIN_LEN"))
     h->global_min_len = std::strtoull(gm, nullptr, 10);
   h->window_cols = window_bytes_for(h->tile_cfg, h->packed) / h->acc_bytes;
+  // replicated x windows for the sparse segments: exact family, Packed16 stream (DG_REPLICAS=0:
+  // column mode only, for A/B)
+  h->slot_mode = h->use_tiles && h->packed && h->accumulation == DG_ACCUM_EXACT;
+  if (const char* rp = std::getenv("DG_REPLICAS")) h->slot_mode = h->slot_mode && std::atoi(rp) != 0;
+  // x staging before the plan: the slot assignment is launched from plan_tiles
+  {
+    const uint64_t n = std::max<uint64_t>(h->cols, 1) + 2 * Handle::kXPad + 32;
+    DG_CUDA(cudaMalloc(&h->d_x_raw, n * sizeof(double)));
+    DG_CUDA(cudaMemset(h->d_x_raw, 0, n * sizeof(double)));
+    DG_CUDA(cudaMalloc(&h->d_x1_raw, n * sizeof(double)));
+    DG_CUDA(cudaMemset(h->d_x1_raw, 0, n * sizeof(double)));
+    h->d_x = h->d_x_raw + Handle::kXPad;
+    h->d_x1 = h->d_x1_raw + Handle::kXPad + 1;
+  }
   DG_TRY(build_plan(h, lens));
   if (h->use_tiles) DG_TRY(plan_tiles(h, lens));
   if (std::getenv("DG_TRACE") && h->use_tiles && h->wave_tiles[0]) {
     h->trace_len = 4ull * h->sm_count + 3ull * h->wave_tiles[0];
     DG_CUDA(cudaMalloc(&h->d_trace, h->trace_len * sizeof(unsigned long long)));
   }
-  // x staging is padded to a 16-byte multiple: the 1-D TMA moves 16-byte granules
-  DG_CUDA(cudaMalloc(&h->d_x, (std::max<uint64_t>(h->cols, 1) + 4) * sizeof(double)));
-  DG_CUDA(cudaMemset(h->d_x, 0, (std::max<uint64_t>(h->cols, 1) + 4) * sizeof(double)));
   DG_CUDA(cudaMalloc(&h->d_y, std::max<uint64_t>(h->rows, 1) * sizeof(double)));
   if (h->accumulation == DG_ACCUM_FP32) {
     DG_CUDA(cudaMalloc(&h->d_xf, (std::max<uint64_t>(h->cols, 1) + 8) * sizeof(float)));
@@ -632,7 +646,8 @@ int dg_destroy(dg_handle* hh) {
   cudaFree(h->d_col);
   cudaFree(h->d_val);
   cudaFree(h->d_packed);
-  cudaFree(h->d_x);
+  cudaFree(h->d_x_raw);
+  cudaFree(h->d_x1_raw);
   cudaFree(h->d_xf);
   cudaFree(h->d_y);
   cudaFree(h->d_bad);
@@ -671,14 +686,23 @@ int dg_dose(dg_handle* hh, const double* x, uint64_t x_len, double* y, uint32_t 
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : h->stream;
   const bool x_dev = flags & DG_X_ON_DEVICE, y_dev = flags & DG_Y_ON_DEVICE;
   // The exact tile kernels TMA the x window straight from the caller's device x when it is
-  // 16-byte aligned with a 16-byte multiple length; otherwise x is staged in the padded buffer.
-  const bool x_direct = x_dev && (reinterpret_cast<uintptr_t>(x) % 16 == 0) && (h->cols % 2 == 0);
+  // 16-byte aligned with a 16-byte multiple length and no window is replicated; otherwise x is
+  // staged in the padded buffers (slot mode also needs the one-element-shifted copy, XSource).
+  if (h->slot_tiles) DG_TRY(dg::recode_slots(h, false));
+  const bool x_direct = x_dev && !h->slot_tiles && (reinterpret_cast<uintptr_t>(x) % 16 == 0) &&
+                        (h->cols % 2 == 0);
   const double* d_x = x_direct ? x : h->d_x;
   double* d_y = y_dev ? y : h->d_y;
   DG_CUDA(cudaEventRecord(h->ev[0], s));
-  if (!x_direct && h->cols)
-    DG_CUDA(cudaMemcpyAsync(h->d_x, x, h->cols * sizeof(double),
-                            x_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+  if (!x_direct && h->cols) {
+    if (!x_dev)
+      DG_CUDA(cudaMemcpyAsync(h->d_x, x, h->cols * sizeof(double), cudaMemcpyHostToDevice, s));
+    if (x_dev || h->slot_tiles) {
+      dg::k_stage_x<<<dg::grid_for(h->cols, 256, 2), 256, 0, s>>>(
+          x_dev ? x : h->d_x, h->d_x, h->slot_tiles ? h->d_x1 : nullptr, h->cols);
+      DG_CUDA(cudaGetLastError());
+    }
+  }
   DG_CUDA(cudaEventRecord(h->ev[1], s));
   h->profiling = (flags & DG_PROFILE) != 0;
   // Host d: download row block k as soon as the tile kernel publishes its completion, while it
@@ -805,6 +829,8 @@ int dg_copy_rows(const dg_handle* hh, uint64_t r0, uint64_t r1, uint64_t* rp_out
   const uint64_t b = rp_out[0], n = rp_out[r1 - r0] - b;
   for (uint64_t i = 0; i <= r1 - r0; ++i) rp_out[i] -= b;
   if (!n) return DG_OK;
+  // slot-mode positions back to columns for the copy (the next dose re-encodes them)
+  DG_TRY(dg::recode_slots(const_cast<Handle*>(h), true));
   uint32_t* d_col = nullptr;
   void* d_val = nullptr;
   DG_CUDA(cudaMalloc(&d_col, n * 4));

@@ -46,6 +46,11 @@ struct Handle {
   static constexpr int kTileUnroll = 8;
   uint32_t acc_bytes = 8;          // shared-memory x element: 8 exact, 4 fp32
   uint32_t window_cols = 0;        // x window capacity per buffer (columns)
+  // replicated x windows (slot mode, spmv_tiles.cuh): exact family on the Packed16 stream
+  bool slot_mode = false;          // the plan may build slot-mode tiles (DG_REPLICAS=0: never)
+  uint32_t rep_stride = 0;         // elements between replica regions of a window buffer
+  uint64_t slot_tiles = 0;         // slot-mode tiles in the plan
+  bool slots_encoded = false;      // the stream's slot-mode positions hold slots (else columns)
   uint64_t tile_nnz = 768 * 1024;  // target nonzeros per tile (finish_create: the measured sweep)
   uint64_t tile_guide = 2;             // guided tail: tiles <= remaining / (guide * SMs) (0: off)
   uint64_t tile_guide_min = 64 * 1024;  // smallest guided tile (nonzeros)
@@ -98,7 +103,13 @@ struct Handle {
   GatherTargets gt = {};
 
   // staging for host x / y and the fp32 family
-  double* d_x = nullptr;
+  // x staged for the tile kernel (XSource): d_x_raw + kXPad is x (16-byte aligned, 16 readable
+  // elements on each side), d_x1_raw + kXPad + 1 the same values one element further on
+  static constexpr uint32_t kXPad = 16;
+  double* d_x_raw = nullptr;
+  double* d_x1_raw = nullptr;
+  double* d_x = nullptr;   // = d_x_raw + kXPad
+  double* d_x1 = nullptr;  // = d_x1_raw + kXPad + 1
   double* d_y = nullptr;
   float* d_xf = nullptr;
   unsigned* d_bad = nullptr;
@@ -182,6 +193,7 @@ int select_device(int32_t want, int* dev_out);
 int check_options(const dg_options* o);
 int finish_create(Handle* h, const std::vector<uint64_t>& lens);
 int plan_tiles(Handle* h, const std::vector<uint64_t>& lens);
+int recode_slots(Handle* h, bool decode);
 int grid_for(uint64_t work_items, int threads, int max_blocks_per_sm = 8);
 
 }  // namespace dg

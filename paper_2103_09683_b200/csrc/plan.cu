@@ -66,6 +66,116 @@ __global__ void k_split_rows(M mat, const uint64_t* __restrict__ rp,
   }
 }
 
+// ---- slot assignment (replicated x windows, spmv_tiles.cuh) ----------------------------------
+// One half-chunk: the <= 16 positions of a segment that one half-warp gathers in one LDS.64.
+// Each position may read its column from any of the kReplicas replicas (bank pair
+// (c - xlo + shift_r) mod 16); masked-off lanes of a partial half read the filler slot 0 (bank
+// pair 0).  Find the replica choice minimising the largest number of distinct words on one bank
+// pair -- the wavefronts that half costs -- by raising the per-bank capacity L from its lower
+// bound until a b-matching of positions to bank pairs exists (BFS augmenting paths; <= 16 x 3
+// edges).  Deterministic: the same stream and plan always give the same slots.
+struct HalfMatch {
+  uint8_t opt[16][kReplicas];  // bank pair per (position, replica)
+  int8_t asg[16];              // replica chosen per position (-1: none yet)
+  uint8_t load[16];
+  int n;
+
+  __device__ int bank(int i) const { return opt[i][asg[i]]; }
+  // one augmenting path from position s under capacities cap[]; false if none
+  __device__ bool augment(int s, const uint8_t* cap) {
+    int8_t via[16];          // via[b]: position that reached bank pair b
+    uint8_t q[16];
+    uint32_t seen_b = 0, seen_p = 1u << s;
+    int qh = 0, qt = 0;
+    q[qt++] = static_cast<uint8_t>(s);
+    int found = -1;
+    while (qh < qt && found < 0) {
+      const int u = q[qh++];
+      for (int r = 0; r < static_cast<int>(kReplicas) && found < 0; ++r) {
+        const int b = opt[u][r];
+        if ((seen_b >> b) & 1u) continue;
+        seen_b |= 1u << b;
+        via[b] = static_cast<int8_t>(u);
+        if (load[b] < cap[b]) { found = b; break; }
+        for (int v = 0; v < n; ++v)
+          if (asg[v] >= 0 && bank(v) == b && !((seen_p >> v) & 1u)) {
+            seen_p |= 1u << v;
+            q[qt++] = static_cast<uint8_t>(v);
+          }
+      }
+    }
+    if (found < 0) return false;
+    int b = found;
+    for (;;) {  // shift every position on the path one step: only `found` gains a word
+      const int u = via[b];
+      const int prev = asg[u] >= 0 ? bank(u) : -1;
+      for (int r = 0; r < static_cast<int>(kReplicas); ++r)
+        if (opt[u][r] == b) { asg[u] = static_cast<int8_t>(r); break; }
+      if (prev < 0) break;
+      b = prev;
+    }
+    ++load[found];
+    return true;
+  }
+  __device__ void solve(bool filler) {
+    for (int L = (n + 15) / 16 > 0 ? (n + 15) / 16 : 1;; ++L) {
+      uint8_t cap[16];
+      for (int b = 0; b < 16; ++b) {
+        cap[b] = static_cast<uint8_t>(L - (filler && b == 0 ? 1 : 0));
+        load[b] = 0;
+      }
+      for (int i = 0; i < n; ++i) asg[i] = -1;
+      bool ok = true;
+      for (int i = 0; i < n && ok; ++i) ok = augment(i, cap);
+      if (ok) return;
+    }
+  }
+};
+
+// decode == 0: rewrite the column field of every position of every slot-mode tile (nrep > 1)
+// into its slot; decode == 1: back to columns (dg_copy_rows, the scatter comparator).
+// One warp per tile, half-chunks strided over its lanes.
+__global__ void k_assign_slots(uint32_t* __restrict__ w, const Tile* __restrict__ tiles,
+                               uint32_t n_tiles, const Segment* __restrict__ segs,
+                               uint32_t stride, int decode) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t n_warps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t t = warp; t < n_tiles; t += n_warps) {
+    const Tile T = tiles[t];
+    if (T.nrep <= 1) continue;
+    for (uint32_t k = T.seg0; k < T.seg1; ++k) {
+      const Segment S = segs[k];
+      const uint64_t base0 = S.p0 - S.lane0;
+      const uint32_t lo = S.lane0, hi = S.lane0 + S.n;
+      const uint32_t halves = (hi + 15) / 16;
+      for (uint32_t u = lo / 16 + lane; u < halves; u += 32) {
+        const uint32_t r0 = u * 16, a = max(r0, lo), e = min(r0 + 16, hi);
+        if (decode) {
+          for (uint32_t rel = a; rel < e; ++rel) {
+            const uint32_t v = w[base0 + rel];
+            w[base0 + rel] = (col_of_slot(v >> 16, T.xlo, stride) << 16) | (v & 0xFFFFu);
+          }
+          continue;
+        }
+        HalfMatch m;
+        m.n = static_cast<int>(e - a);
+        uint32_t col[16];
+        for (int i = 0; i < m.n; ++i) {
+          col[i] = w[base0 + a + i] >> 16;
+          for (uint32_t r = 0; r < kReplicas; ++r)
+            m.opt[i][r] = static_cast<uint8_t>((col[i] - T.xlo + rep_shift(r)) & 15u);
+        }
+        m.solve(e - a < 16);
+        for (int i = 0; i < m.n; ++i) {
+          const uint32_t v = w[base0 + a + i];
+          w[base0 + a + i] = (slot_of(col[i], T.xlo, m.asg[i], stride) << 16) | (v & 0xFFFFu);
+        }
+      }
+    }
+  }
+}
+
 namespace {
 
 struct HostSeg {
@@ -84,6 +194,17 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
   // windows below (stride W - A); dense rows may span a whole window (their lanes read
   // consecutive x, so they share a window with few others anyway)
   const uint32_t A = (W / 3) / align * align;
+  // slot mode (replicated windows, exact family on the Packed16 stream): kReplicas replica
+  // regions of RS = W / kReplicas elements per buffer; a slot-mode window spans W3 columns (room
+  // for the largest replica shift and 16-byte rounding) and takes the sparse segments spanning
+  // <= A3 columns (C2: every sparse row, whose columns lie in a 4,096-column locality window),
+  // binned on a grid of stride W3 - A3.
+  const bool rep = h->slot_mode;
+  const uint32_t RS = W / kReplicas;
+  const uint32_t W3 = (RS - 16) / 16 * 16;
+  const uint32_t A3 = W3 >= 4096u + 256u ? 4096u : W3 * 2 / 3 / align * align;
+  const uint32_t St3 = W3 - A3;
+  h->rep_stride = RS;
   std::vector<uint64_t> rp(rows + 1, 0);
   for (uint64_t r = 0; r < rows; ++r) rp[r + 1] = rp[r] + lens[r];
 
@@ -304,7 +425,7 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     };
     // signalled when one launch finishes every row: a single wave, or fused waves (a block
     // completes with the last of its tiles in any wave)
-    const uint16_t blk = NW == 1 || h->fused_waves ? static_cast<uint16_t>(k) : kNoBlock;
+    const uint8_t blk = NW == 1 || h->fused_waves ? static_cast<uint8_t>(k) : kNoBlock;
     const size_t tiles_before = tiles.size();
     auto take = [&](const HostSeg& q) {
       segs.push_back({q.p0, q.n, q.row, q.slot, q.lane0, q.flags});
@@ -326,7 +447,7 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
           nnz += G[g].n;
           take(G[g++]);
         }
-        tiles.push_back({0, 0, blk, s0, static_cast<uint32_t>(segs.size())});
+        tiles.push_back({0, 0, blk, 1, s0, static_cast<uint32_t>(segs.size())});
       }
     }
     // windowed tiles.  Narrow segments (span <= A = W/3) are binned into a fixed grid of windows
@@ -334,15 +455,30 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     // fits window g, so the rare wide segments (e.g. a row's clusters in two adjacent beams,
     // merged into one segment) cannot cut the tiles of narrow ones short.  Wide segments are
     // packed greedily in first-column order.  Each bin: first-column order, cut at ~cap nonzeros.
+    // windowed tiles, three classes: (0) slot-mode: sparse segments spanning <= A3 columns,
+    // binned on the grid [g*St3, g*St3 + W3) of replicated windows; (1) narrow: segments spanning
+    // <= A = W/3, binned into a fixed grid of windows [g*St, g*St + W), stride St = W - A -- a
+    // segment whose first column lies in [g*St, (g+1)*St) fits window g, so the rare wide
+    // segments (e.g. a row's clusters in two adjacent beams, merged into one segment) cannot cut
+    // the tiles of narrow ones short; (2) wide: packed greedily in first-column order.  Each bin:
+    // first-column order, cut at ~cap nonzeros.
     auto& S = win[w][k];
+    auto cls = [&](const HostSeg& q) -> int {
+      const uint32_t span = q.chi - q.clo + 1;
+      if (rep && span <= A3 && 4ull * q.n < 3ull * span) return 0;
+      return narrow(q) ? 1 : 2;
+    };
+    auto bin = [&](const HostSeg& q, int c) -> uint32_t {
+      return c == 0 ? q.clo / St3 : c == 1 ? q.clo / St : 0;
+    };
     std::stable_sort(S.begin(), S.end(), [&](const HostSeg& a, const HostSeg& b) {
-      const bool na = narrow(a), nb = narrow(b);
-      if (na != nb) return na;
-      const uint32_t ga = na ? a.clo / St : 0, gb = nb ? b.clo / St : 0;
+      const int ca = cls(a), cb = cls(b);
+      if (ca != cb) return ca < cb;
+      const uint32_t ga = bin(a, ca), gb = bin(b, cb);
       if (ga != gb) return ga < gb;
       return a.clo != b.clo ? a.clo < b.clo : a.row < b.row;
     });
-    auto emit = [&](size_t i, size_t j) {
+    auto emit = [&](size_t i, size_t j, uint8_t nrep) {
       uint32_t lo = S[i].clo, hi = S[i].chi;
       for (size_t q = i; q < j; ++q) {
         lo = std::min(lo, S[q].clo);
@@ -354,20 +490,23 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
                        [](const HostSeg& a, const HostSeg& b) { return a.n > b.n; });
       uint32_t xlen = (hi - xlo + 1 + align - 1) / align * align;
       if (xlo + xlen > xcap) xlen = static_cast<uint32_t>(xcap - xlo);
-      tiles.push_back({xlo, static_cast<uint16_t>(xlen), blk, static_cast<uint32_t>(segs.size()),
+      tiles.push_back({xlo, static_cast<uint16_t>(xlen), blk, nrep,
+                       static_cast<uint32_t>(segs.size()),
                        static_cast<uint32_t>(segs.size() + (j - i))});
       for (size_t q = i; q < j; ++q) take(S[q]);
     };
     size_t i = 0;
-    while (i < S.size() && narrow(S[i])) {  // narrow: per grid window, cut by nonzeros
-      const uint32_t g = S[i].clo / St;
-      uint64_t nnz = 0;
-      size_t j = i;
-      const uint64_t cap = cap_nnz();
-      while (j < S.size() && narrow(S[j]) && S[j].clo / St == g && (j == i || nnz + S[j].n <= cap))
-        nnz += S[j++].n;
-      emit(i, j);
-      i = j;
+    for (int c = 0; c < 2; ++c) {  // binned classes: per grid window, cut by nonzeros
+      while (i < S.size() && cls(S[i]) == c) {
+        const uint32_t g = bin(S[i], c);
+        uint64_t nnz = 0;
+        size_t j = i;
+        const uint64_t cap = cap_nnz();
+        while (j < S.size() && cls(S[j]) == c && bin(S[j], c) == g && (j == i || nnz + S[j].n <= cap))
+          nnz += S[j++].n;
+        emit(i, j, c == 0 ? static_cast<uint8_t>(kReplicas) : 1);
+        i = j;
+      }
     }
     while (i < S.size()) {  // wide: greedy, cut at the window width or ~cap nonzeros
       const uint32_t xlo = S[i].clo / align * align;
@@ -382,7 +521,7 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
         nnz += S[j].n;
         ++j;
       }
-      emit(i, j);
+      emit(i, j, 1);
       i = j;
     }
     if (blk != kNoBlock) h->blk_tiles[k] += static_cast<uint32_t>(tiles.size() - tiles_before);
@@ -417,7 +556,9 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     DG_CUDA(cudaMemcpy(h->d_segs[lw], segs.data(), segs.size() * sizeof(Segment),
                        cudaMemcpyHostToDevice));
     h->plan_bytes += tiles.size() * sizeof(Tile) + segs.size() * sizeof(Segment);
+    for (const Tile& t : tiles) h->slot_tiles += t.nrep > 1;
   }
+  if (h->slot_tiles) DG_TRY(recode_slots(h, false));
   if (h->n_carry_slots) {
     const uint64_t n = h->n_carry_slots * 32;
     DG_CUDA(cudaMalloc(&h->d_state, n * h->acc_bytes));
@@ -439,6 +580,23 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
 }
 
 }  // namespace
+
+// Rewrite the slot-mode tiles' positions of the Packed16 stream between columns (decode) and
+// slots (encode); the handle remembers which form the stream is in.
+int recode_slots(Handle* h, bool decode) {
+  if (!h->slot_tiles || h->slots_encoded == !decode) return DG_OK;
+  const uint32_t NL = h->fused_waves ? 1 : h->n_waves;
+  for (uint32_t lw = 0; lw < NL; ++lw) {
+    if (!h->wave_tiles[lw]) continue;
+    k_assign_slots<<<grid_for(32ull * h->wave_tiles[lw], 128, 16), 128>>>(
+        h->d_packed, static_cast<const Tile*>(h->d_tiles[lw]), h->wave_tiles[lw],
+        static_cast<const Segment*>(h->d_segs[lw]), h->rep_stride, decode ? 1 : 0);
+    DG_CUDA(cudaGetLastError());
+  }
+  DG_CUDA(cudaDeviceSynchronize());
+  h->slots_encoded = !decode;
+  return DG_OK;
+}
 
 int plan_tiles(Handle* h, const std::vector<uint64_t>& lens) {
   return dispatch_mat(h, [&](const auto& mat) { return plan_tiles_typed(h, mat, lens); });

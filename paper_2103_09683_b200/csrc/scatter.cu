@@ -162,6 +162,7 @@ int dg_scatter_create(const dg_csr_view* v, uint32_t chunk_count, int32_t device
   cu(cudaMalloc(&keys_out, nz * 4));
   cu(cudaMalloc(&idx, nz * 4));
   cu(cudaMalloc(&perm, nz * 4));
+  if (st == DG_OK) st = dg::recode_slots(h, true);  // columns, not slots (the next dose re-encodes)
   if (st == DG_OK) {
     cu(cudaMemset(s->d_col_ptr, 0, (s->cols + 1) * 8));
     dg::k_row_of<<<dg::grid_for(s->rows, 256), 256>>>(h->d_row_ptr, s->rows, r_of);

@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(256) k_group(M mat, const uint64_t* __restrict
                                                const Acc* __restrict__ x,
                                                const uint32_t* __restrict__ rows,
                                                uint32_t n_rows, double* __restrict__ y,
-                                               GatherTargets gt) {
+                                               const __grid_constant__ GatherTargets gt) {
   using Ops = AccOps<Acc>;
   const uint32_t lane = threadIdx.x & (G - 1);
   const uint64_t group = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / G;
@@ -73,7 +73,7 @@ template <class M, typename Acc>
 __global__ void __launch_bounds__(256) k_warp(M mat, const uint64_t* __restrict__ rp,
                                               const Acc* __restrict__ x,
                                               const uint32_t* __restrict__ rows, uint32_t n_rows,
-                                              double* __restrict__ y, GatherTargets gt) {
+                                              double* __restrict__ y, const __grid_constant__ GatherTargets gt) {
   using Ops = AccOps<Acc>;
   constexpr int U = 8;
   const uint32_t lane = threadIdx.x & 31;
@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(256) k_warp(M mat, const uint64_t* __restrict_
 template <class M>
 __global__ void k_block_exact(M mat, const uint64_t* __restrict__ rp, const double* __restrict__ x,
                               const uint32_t* __restrict__ rows, uint32_t n_rows,
-                              double* __restrict__ y, GatherTargets gt) {
+                              double* __restrict__ y, const __grid_constant__ GatherTargets gt) {
   extern __shared__ double partial[];
   const uint32_t L = blockDim.x, l = threadIdx.x;
   for (uint32_t b = blockIdx.x; b < n_rows; b += gridDim.x) {

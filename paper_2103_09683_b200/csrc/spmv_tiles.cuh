@@ -123,10 +123,34 @@ __global__ void k_carry_init(Acc* __restrict__ state, uint64_t n) {
 struct Tile {  // 16 bytes
   uint32_t xlo;   // x window start (16-byte aligned)
   uint16_t xlen;  // x window length in elements (16-byte multiple; 0: global-x tile)
-  uint16_t blk;   // output row block whose rows this tile finishes (kNoBlock: none)
+  uint8_t blk;    // output row block whose rows this tile finishes (kNoBlock: none)
+  uint8_t nrep;   // x replicas in the window: 1 (column mode) or kReplicas (slot mode)
   uint32_t seg0, seg1;
 };
-constexpr uint16_t kNoBlock = 0xFFFF;
+constexpr uint8_t kNoBlock = 0xFF;
+
+// ---- replicated x windows (slot mode) -------------------------------------------------------
+// A warp's 8-byte x gather is served half-warp by half-warp, each half in as many shared-memory
+// wavefronts as the most-loaded of the 16 bank pairs (distinct words; scripts/micro/lds_model.cu
+// measured it on B200).  Sparse rows gather random columns, so a half-warp's 16 columns land on
+// ~2.45 words per bank pair at worst on average: 4.9 wavefronts per 32 nonzeros instead of 2
+// (r01 ncu: 41% of the kernel's shared wavefronts were conflicts).  A slot-mode tile holds its
+// x window kReplicas times, replica r shifted by kRepShift[r] bank pairs, and the plan rewrites
+// each nonzero's 16-bit column of the Packed16 stream into the *slot* it gathers from: replica
+// chosen per nonzero so that every half-warp's lanes spread over the bank pairs with the smallest
+// possible maximum load (an exact b-matching per half-chunk, k_assign_slots in plan.cu).  Same
+// 4 bytes per nonzero; the column is recovered from (tile.xlo, slot) -- the decode is exact.
+constexpr uint32_t kReplicas = 3;
+__host__ __device__ constexpr uint32_t rep_shift(uint32_t r) { return r == 0 ? 0u : r == 1 ? 4u : 11u; }
+// slot of column c in replica r of a window starting at xlo, replica regions `stride` apart
+__host__ __device__ __forceinline__ uint32_t slot_of(uint32_t c, uint32_t xlo, uint32_t r,
+                                                     uint32_t stride) {
+  return r * stride + (c - xlo) + rep_shift(r);
+}
+__host__ __device__ __forceinline__ uint32_t col_of_slot(uint32_t slot, uint32_t xlo, uint32_t stride) {
+  const uint32_t r = slot / stride;
+  return xlo + (slot - r * stride) - rep_shift(r);
+}
 
 // Row-block completion signals: the CTA finishing the last tile of output row block k publishes
 // flag[k] = epoch, which a copy stream waits on (cuStreamWaitValue32) to move block k of d to the
@@ -185,11 +209,14 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
 
 // x sources: the tile's shared-memory window, or global x (L1/L2) for dense wide rows whose
 // column span exceeds a window (kSegGlobalX) -- their 32 lanes read 32 consecutive x entries.
+// The window is indexed by the stream's 16-bit field directly: `base` is the buffer minus xlo in
+// column mode (field = column) and the buffer itself in slot mode (field = slot); `safe` is a
+// valid field value for masked-off lanes.
 template <typename Acc>
 struct XWindow {
-  const Acc* xs;
-  uint32_t xlo;
-  __device__ __forceinline__ Acc operator()(uint32_t c) const { return xs[c - xlo]; }
+  const Acc* base;
+  uint32_t safe;
+  __device__ __forceinline__ Acc operator()(uint32_t c) const { return base[c]; }
 };
 template <typename Acc>
 struct XGlobal {
@@ -340,7 +367,7 @@ __device__ __forceinline__ void run_segments(const M& mat, const XWindow<Acc>& x
   bool have_next = grab(sn);
   Acc carried_next = PEEK && have_next ? carry.peek(sn.slot, sn.flags, lane) : Acc(0);
   Raw ra[U], rb[U];
-  const uint32_t safe = xw.xlo;
+  const uint32_t safe = xw.safe;
   uint32_t ma = load_batch<U>(mat, ra, cur, 0, lane, safe), mb = 0;
   prefetch_batches<U, P>(mat, cur, 1, lane);
   bool sn_pf = false;  // the next segment's head (P + 1 batches) has been prefetched
@@ -406,7 +433,7 @@ template <class M, typename Acc, int U, int P>
 __global__ void __launch_bounds__(256)
     k_dense(M mat, const uint64_t* __restrict__ rp, const Acc* __restrict__ x,
             const uint32_t* __restrict__ rows, uint32_t n_rows, uint32_t* __restrict__ counter,
-            double* __restrict__ y, GatherTargets gt) {
+            double* __restrict__ y, const __grid_constant__ GatherTargets gt) {
   using Ops = AccOps<Acc>;
   using Raw = typename M::Raw;
   // programmatic dependent launch: the tile kernel that follows may take each SM as soon as
@@ -471,145 +498,35 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// ---- TMA ring variant (Packed16): each warp streams its segments' batches into a private ring
-// of R shared-memory stages with 1-D bulk copies issued by lane 0, so R-1 batches (~1 KB each)
-// are in flight per warp without holding registers.  Stage t carries a copy of its batch's
-// descriptor; batches are consumed in issue order, which is segment order, which is lane-partial
-// order -- so the accumulation order is exactly the register pipeline's.
-constexpr uint32_t kStageElems = 264;  // 256 positions + up to 3 + 3 alignment slack, x 4 B
-
-struct StageMeta {
-  uint64_t base0;
-  uint32_t lo, hi, k, nbatch, row, slot, flags, al;  // al: element offset of stage[0] from base0
-};
-
-template <int U, int R, typename Acc, class GrabFn>
-__device__ __forceinline__ void run_segments_tma(const Packed16& mat, const XWindow<Acc>& xw,
-                                                 const XGlobal<Acc>& xg, GrabFn&& grab,
-                                                 const Carry<Acc>& carry, double* __restrict__ y,
-                                                 const GatherTargets& gt,
-                                                 uint32_t lane, uint32_t* ring, StageMeta* meta,
-                                                 uint64_t* bars, uint32_t& parity) {
-  static_assert(U * 32 == 256, "stage layout assumes 256-position batches");
-  using Ops = AccOps<Acc>;
-  // producer cursor: meaningful in lane 0 only
-  SegRun pseg{};
-  uint32_t pk = 0;
-  Segment pre{};
-  bool have_pre = false, have_cur = false;
-  {
-    Segment s0;
-    if (grab(s0)) {
-      pseg = seg_run<U>(s0);
-      have_cur = true;
-      have_pre = grab(pre);
-    }
-  }
-  // issue the next batch into stage t; returns whether anything was issued (warp-uniform)
-  auto issue = [&](int t) -> bool {
-    if (have_cur && pk == pseg.nbatch) {
-      have_cur = have_pre;
-      if (have_cur) {
-        pseg = seg_run<U>(pre);
-        pk = 0;
-        have_pre = grab(pre);
-      }
-    }
-    if (!have_cur) return false;
-    if (lane == 0) {
-      const uint32_t b0 = pk * 256u;
-      const uint32_t rs = max(pseg.lo, b0), re = min(pseg.hi, b0 + 256u);
-      const uint64_t start = pseg.base0 + rs, end = pseg.base0 + re;
-      const uint64_t lo_al = start & ~3ull, hi_al = (end + 3) & ~3ull;
-      StageMeta m;
-      m.base0 = pseg.base0;
-      m.lo = pseg.lo;
-      m.hi = pseg.hi;
-      m.k = pk;
-      m.nbatch = pseg.nbatch;
-      m.row = pseg.row;
-      m.slot = pseg.slot;
-      m.flags = pseg.flags;
-      m.al = static_cast<uint32_t>(lo_al - pseg.base0);
-      meta[t] = m;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // WAR on ring[t]
-      const uint32_t bytes = static_cast<uint32_t>(hi_al - lo_al) * 4u;
-      mbar_arrive_expect_tx(&bars[t], bytes);
-      tma_load_1d(ring + t * kStageElems, mat.w + lo_al, bytes, &bars[t]);
-    }
-    ++pk;
-    return true;
-  };
-  int inflight = 0;
-#pragma unroll
-  for (int t = 0; t < R; ++t)
-    if (issue(t)) ++inflight;
-  Acc acc = Acc(0);
-  int cs = 0;
-  while (inflight > 0) {
-    mbar_wait(&bars[cs], (parity >> cs) & 1u);
-    parity ^= 1u << cs;
-    const StageMeta m = meta[cs];
-    if (m.k == 0)
-      acc = carry.in(m.slot, m.flags, lane);
-    const uint32_t* st = ring + cs * kStageElems;
-    uint32_t raw[U];
-    uint32_t mask = 0;
-    const uint32_t b0 = m.k * 256u + lane;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint32_t rel = b0 + 32 * u;
-      const bool ok = rel >= m.lo && rel < m.hi;
-      raw[u] = ok ? st[rel - m.al] : Packed16::filler(xw.xlo);
-      mask |= static_cast<uint32_t>(ok) << u;
-    }
-    if (m.flags & kSegGlobalX) consume_batch<U, Packed16>(raw, mask, xg, acc);
-    else consume_batch<U, Packed16>(raw, mask, xw, acc);
-    if (m.k + 1 == m.nbatch) {
-      if (m.flags & kSegLast) {
-#pragma unroll
-        for (int off = 16; off >= 1; off /= 2) acc = Ops::add(acc, __shfl_down_sync(kFull, acc, off));
-        if (lane == 0) {
-          y[m.row] = static_cast<double>(acc);
-          gt.store(m.row, static_cast<double>(acc));
-        }
-      } else {
-        carry.out(m.slot, m.flags, lane, acc);
-      }
-    }
-    --inflight;
-    __syncwarp();  // every lane is done reading stage cs before it is refilled
-    if (issue(cs)) ++inflight;
-    cs = cs + 1 == R ? 0 : cs + 1;
-  }
-}
-
-// Shared memory of k_tiles beyond the two x-window buffers.
-template <int WARPS, int R>
-constexpr size_t ring_smem_bytes() {
-  return R > 0 ? static_cast<size_t>(WARPS) * R * (kStageElems * 4 + sizeof(StageMeta) + 8) : 0;
-}
-
-// Persistent: one CTA per SM; dynamic smem = 2 * wcap * sizeof(Acc) (two x-window buffers)
-// + ring_smem_bytes<WARPS, R>() (R > 0: TMA-streamed matrix, Packed16 only).
+// Persistent: one CTA per SM; dynamic smem = NB * wcap * sizeof(Acc) (the x-window buffers).
 #ifndef DG_PREFETCH_SEGS
 #define DG_PREFETCH_SEGS 1
 #endif
 constexpr bool kPrefetchSegs = DG_PREFETCH_SEGS;
 
+// x as the tile kernel reads it: `x` (16-byte aligned, readable 16 elements before x[0] and past
+// x[cols - 1]) and `x1`, the same values one element further on (x1 + i holds x[i] at an address
+// 8 bytes off x's 16-byte phase), so a replica with an odd bank shift is still one 16-byte-aligned
+// bulk copy.  `rep_stride`: elements between the replica regions of a window buffer.
+template <typename Acc>
+struct XSource {
+  const Acc* x;
+  const Acc* x1;
+  uint32_t rep_stride;
+};
 
-template <class M, typename Acc, int WARPS, int U, int R = 0, int P = 0, int NB = 2,
-          bool CARRY = true>
+template <class M, typename Acc, int WARPS, int U, int P = 0, int NB = 2, bool CARRY = true>
 __global__ void __launch_bounds__(WARPS * 32, 1)
-    k_tiles(M mat, const Acc* __restrict__ x, const Tile* __restrict__ tiles, uint32_t n_tiles,
+    k_tiles(M mat, XSource<Acc> xsrc, const Tile* __restrict__ tiles, uint32_t n_tiles,
             const Segment* __restrict__ segs, Carry<Acc> carry, double* __restrict__ y,
-            uint32_t* __restrict__ counter, uint32_t wcap, BlockSignal sig, GatherTargets gt,
+            uint32_t* __restrict__ counter, uint32_t wcap, BlockSignal sig, const __grid_constant__ GatherTargets gt,
             TileTrace tr) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[NB];
   __shared__ uint32_t tile_of[NB], seg_next[NB], done[NB];
   Acc* const xbuf0 = reinterpret_cast<Acc*>(smem_raw);
   const uint32_t lane = threadIdx.x & 31;
+  const Acc* __restrict__ x = xsrc.x;
 
   // claim the next tile for buffer b and start its window transfer (one thread)
   auto refill = [&](int b) {
@@ -626,12 +543,33 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       }
       // order earlier generic-proxy reads of this buffer before the async-proxy overwrite
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      const uint32_t bytes = T.xlen * static_cast<uint32_t>(sizeof(Acc));  // 0: global-x tile
-      mbar_arrive_expect_tx(&full[b], bytes);
-      const char* src = reinterpret_cast<const char*>(x + T.xlo);
-      char* dst = reinterpret_cast<char*>(xbuf0 + b * wcap);
-      for (uint32_t off = 0; off < bytes; off += 32768u)
-        tma_load_1d(dst + off, src + off, min(32768u, bytes - off), &full[b]);
+      char* const dst0 = reinterpret_cast<char*>(xbuf0 + b * wcap);
+      if (T.nrep <= 1) {
+        const uint32_t bytes = T.xlen * static_cast<uint32_t>(sizeof(Acc));  // 0: global-x tile
+        mbar_arrive_expect_tx(&full[b], bytes);
+        const char* src = reinterpret_cast<const char*>(x + T.xlo);
+        for (uint32_t off = 0; off < bytes; off += 32768u)
+          tma_load_1d(dst0 + off, src + off, min(32768u, bytes - off), &full[b]);
+      } else {
+        // replica r: elements [xlo - shift_r, xlo - shift_r + len_r) at dst + r * stride, so
+        // column c sits at slot r * stride + (c - xlo) + shift_r (slot_of)
+        constexpr uint32_t kAl = 16 / sizeof(Acc);
+        uint32_t total = 0;
+#pragma unroll
+        for (uint32_t r = 0; r < kReplicas; ++r)
+          total += (T.xlen + rep_shift(r) + kAl - 1) / kAl * kAl * static_cast<uint32_t>(sizeof(Acc));
+        mbar_arrive_expect_tx(&full[b], total);
+#pragma unroll
+        for (uint32_t r = 0; r < kReplicas; ++r) {
+          const uint32_t sh = rep_shift(r);
+          const uint32_t bytes = (T.xlen + sh + kAl - 1) / kAl * kAl * static_cast<uint32_t>(sizeof(Acc));
+          const Acc* base = (sh & 1u) ? xsrc.x1 : x;
+          const char* src = reinterpret_cast<const char*>(base + T.xlo) - sh * sizeof(Acc);
+          char* dst = dst0 + static_cast<size_t>(r) * xsrc.rep_stride * sizeof(Acc);
+          for (uint32_t off = 0; off < bytes; off += 32768u)
+            tma_load_1d(dst + off, src + off, min(32768u, bytes - off), &full[b]);
+        }
+      }
       // the tile's segment descriptors into L2 (one bulk prefetch): the warps' grabs then wait
       // on an L2 hit, not DRAM -- short segments need the next descriptor almost at once
       const uint64_t sb = reinterpret_cast<uint64_t>(segs + T.seg0) & ~15ull;
@@ -645,23 +583,6 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     }
   };
 
-  // TMA ring carve-up (R > 0): per warp R stages, R stage descriptors, R mbarriers
-  const uint32_t warp = threadIdx.x >> 5;
-  uint32_t* my_ring = nullptr;
-  StageMeta* my_meta = nullptr;
-  uint64_t* my_bars = nullptr;
-  uint32_t ring_parity = 0;
-  if constexpr (R > 0) {
-    unsigned char* p = smem_raw + static_cast<size_t>(NB) * wcap * sizeof(Acc);
-    uint32_t* rings = reinterpret_cast<uint32_t*>(p);
-    StageMeta* metas = reinterpret_cast<StageMeta*>(p + WARPS * R * kStageElems * 4);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(p + WARPS * R * kStageElems * 4 +
-                                                 WARPS * R * sizeof(StageMeta));
-    my_ring = rings + warp * R * kStageElems;
-    my_meta = metas + warp * R;
-    my_bars = bars + warp * R;
-    if (lane < R) mbar_init(&my_bars[lane], 1);
-  }
   if (threadIdx.x == 0) {
     for (int i = 0; i < NB; ++i) mbar_init(&full[i], 1);
   }
@@ -688,7 +609,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     const uint32_t t = *reinterpret_cast<volatile uint32_t*>(&tile_of[b]);
     if (t >= n_tiles) break;
     const Tile T = tiles[t];
-    const XWindow<Acc> xw{xbuf0 + b * wcap, T.xlo};
+    const bool slots = T.nrep > 1;
+    const XWindow<Acc> xw{xbuf0 + b * wcap - (slots ? 0u : T.xlo), slots ? 0u : T.xlo};
     const XGlobal<Acc> xg{x};
     const uint32_t nseg = T.seg1 - T.seg0;
     auto grab = [&](Segment& s) -> bool {
@@ -699,14 +621,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       s = segs[T.seg0 + k];
       return true;
     };
-    if constexpr (R > 0) {
-      run_segments_tma<U, R>(mat, xw, xg, grab, carry, y, gt, lane, my_ring, my_meta, my_bars,
-                             ring_parity);
-    } else {
-      // peek only with >= 96 registers per thread
-      constexpr bool kPeek = CARRY && WARPS * 32 * 96 <= 65536;
-      run_segments<U, P, CARRY, kPeek>(mat, xw, xg, grab, carry, y, gt, lane);
-    }
+    // peek only with >= 96 registers per thread
+    constexpr bool kPeek = CARRY && WARPS * 32 * 96 <= 65536;
+    run_segments<U, P, CARRY, kPeek>(mat, xw, xg, grab, carry, y, gt, lane);
     __syncwarp();
     if (lane == 0) {
       // this warp's reads of buffer b (and, when signalling, its d stores) happen before the count
