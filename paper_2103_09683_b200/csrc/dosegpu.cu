@@ -307,6 +307,7 @@ int launch_tiles(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t 
   //  per SM -- C2 3.89 ms vs 2.88 back to back; profiles/README.md)
   DG_TRY(launch_dense(h, mat, x, y, s));
   if (!h->n_waves) return DG_OK;
+  if (h->slices) return launch_slices<Acc>(h, x, y, s);
   constexpr int kP = std::is_same_v<Acc, float> ? 4 : 2;  // measured: prefetch distance
   if constexpr (std::is_same_v<M, Packed16>) {
     switch (h->tile_cfg) {
@@ -457,8 +458,12 @@ int finish_create(Handle* h, const std::vector<uint64_t>& lens) {
   h->window_cols = window_bytes_for(h->tile_cfg, h->packed) / h->acc_bytes;
   // replicated x windows for the sparse segments: exact family, Packed16 stream (DG_REPLICAS=0:
   // column mode only, for A/B)
-  h->slot_mode = h->use_tiles && h->packed && h->accumulation == DG_ACCUM_EXACT;
+  h->slot_mode = h->use_tiles && h->value_precision == DG_HALF && h->accumulation == DG_ACCUM_EXACT;
   if (const char* rp = std::getenv("DG_REPLICAS")) h->slot_mode = h->slot_mode && std::atoi(rp) != 0;
+  // the slice stream: binary16 values (Packed16 or U32 SoA uploads), k_dense available
+  h->slices_wanted = h->use_tiles && h->value_precision == DG_HALF && h->dense_mode != 0;
+  if (const char* sl = std::getenv("DG_SLICES")) h->slices_wanted = h->slices_wanted && std::atoi(sl) != 0;
+  h->slot_mode = h->slot_mode && (h->packed || h->slices_wanted);
   // x staging before the plan: the slot assignment is launched from plan_tiles
   {
     const uint64_t n = std::max<uint64_t>(h->cols, 1) + 2 * Handle::kXPad + 32;
@@ -471,6 +476,7 @@ int finish_create(Handle* h, const std::vector<uint64_t>& lens) {
   }
   DG_TRY(build_plan(h, lens));
   if (h->use_tiles) DG_TRY(plan_tiles(h, lens));
+  DG_TRY(build_slices(h));
   if (std::getenv("DG_TRACE") && h->use_tiles && h->wave_tiles[0]) {
     h->trace_len = 4ull * h->sm_count + 3ull * h->wave_tiles[0];
     DG_CUDA(cudaMalloc(&h->d_trace, h->trace_len * sizeof(unsigned long long)));
@@ -640,6 +646,10 @@ int dg_destroy(dg_handle* hh) {
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   cudaFree(h->d_row_ptr);
+  cudaFree(h->d_row_ptr_orig);
+  cudaFree(h->d_slices);
+  cudaFree(h->d_ranges);
+  cudaFree(h->d_sseg);
   cudaFree(h->d_trace);
   cudaFree(h->d_dense_rows);
   cudaFree(h->d_dense_counter);
@@ -816,7 +826,7 @@ int dg_copy_row_ptr(const dg_handle* hh, uint64_t r0, uint64_t r1, uint64_t* rp_
   const Handle* h = reinterpret_cast<const Handle*>(hh);
   if (!h || !rp_out || r0 > r1 || r1 > h->rows) return DG_ERR_INVALID_CONFIG;
   DG_CUDA(cudaSetDevice(h->device));
-  DG_CUDA(cudaMemcpy(rp_out, h->d_row_ptr + r0, (r1 - r0 + 1) * 8, cudaMemcpyDeviceToHost));
+  DG_CUDA(cudaMemcpy(rp_out, dg::orig_row_ptr(h) + r0, (r1 - r0 + 1) * 8, cudaMemcpyDeviceToHost));
   return DG_OK;
 }
 
@@ -825,10 +835,25 @@ int dg_copy_rows(const dg_handle* hh, uint64_t r0, uint64_t r1, uint64_t* rp_out
   const Handle* h = reinterpret_cast<const Handle*>(hh);
   if (!h || r0 > r1 || r1 > h->rows) return DG_ERR_INVALID_CONFIG;
   DG_CUDA(cudaSetDevice(h->device));
-  DG_CUDA(cudaMemcpy(rp_out, h->d_row_ptr + r0, (r1 - r0 + 1) * 8, cudaMemcpyDeviceToHost));
+  DG_CUDA(cudaMemcpy(rp_out, dg::orig_row_ptr(h) + r0, (r1 - r0 + 1) * 8, cudaMemcpyDeviceToHost));
   const uint64_t b = rp_out[0], n = rp_out[r1 - r0] - b;
   for (uint64_t i = 0; i <= r1 - r0; ++i) rp_out[i] -= b;
   if (!n) return DG_OK;
+  if (h->slices) {  // decode the slice and rest streams back to the row-ordered encoding
+    uint32_t* d_col = nullptr;
+    uint16_t* d_val = nullptr;
+    DG_CUDA(cudaMalloc(&d_col, n * 4));
+    cudaError_t e = cudaMalloc(&d_val, n * 2);
+    int st = e == cudaSuccess ? dg::decode_rows(h, r0, r1, d_col, d_val) : DG_ERR_CUDA_BASE + (int)e;
+    if (st == DG_OK) {
+      e = cudaMemcpy(col_out, d_col, n * 4, cudaMemcpyDeviceToHost);
+      if (e == cudaSuccess) e = cudaMemcpy(val_out, d_val, n * 2, cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) st = DG_ERR_CUDA_BASE + (int)e;
+    }
+    cudaFree(d_col);
+    cudaFree(d_val);
+    return st;
+  }
   // slot-mode positions back to columns for the copy (the next dose re-encodes them)
   DG_TRY(dg::recode_slots(const_cast<Handle*>(h), true));
   uint32_t* d_col = nullptr;

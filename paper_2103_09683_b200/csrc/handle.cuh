@@ -12,6 +12,9 @@
 
 namespace dg {
 
+struct Tile;
+struct Segment;
+
 constexpr int kNumBins = 8;
 constexpr int kBinLong = 6;     // v0 plan (DG_PLAN=warp): rows with len > 32, warp per row
 constexpr int kBinGeneral = 7;  // L != 32: every non-empty row
@@ -51,6 +54,21 @@ struct Handle {
   uint32_t rep_stride = 0;         // elements between replica regions of a window buffer
   uint64_t slot_tiles = 0;         // slot-mode tiles in the plan
   bool slots_encoded = false;      // the stream's slot-mode positions hold slots (else columns)
+  // slice stream (spmv_slices.cuh, slices.cu): binary16 matrices under lane_width 32
+  static constexpr int kSliceWarps = 32;       // warps per CTA of k_slices
+  static constexpr int kSliceWarpsCarry = 20;  // ... with carried partials (split rows)
+  bool slices_wanted = false;      // plan for the slice stream (DG_SLICES=0: row-ordered k_tiles)
+  bool slices = false;             // the plan has one; d_slices holds it
+  int slice_warps = 0;
+  uint64_t slice_chunks = 0;       // 32-word chunks in the stream
+  uint32_t* d_slices = nullptr;
+  void* d_ranges = nullptr;        // WarpRange[tiles * warps + 1]
+  void* d_sseg = nullptr;          // SliceSeg per segment
+  uint64_t n_segments = 0;         // segments of launch list 0
+  // with slices the handle's stream (d_packed / d_col / d_val, d_row_ptr) is the REST stream of
+  // the rows the tile kernel does not own; d_row_ptr_orig is the upload's row pointer
+  uint64_t* d_row_ptr_orig = nullptr;
+  uint64_t rest_nnz = 0;
   uint64_t tile_nnz = 768 * 1024;  // target nonzeros per tile (finish_create: the measured sweep)
   uint64_t tile_guide = 2;             // guided tail: tiles <= remaining / (guide * SMs) (0: off)
   uint64_t tile_guide_min = 64 * 1024;  // smallest guided tile (nonzeros)
@@ -194,6 +212,13 @@ int check_options(const dg_options* o);
 int finish_create(Handle* h, const std::vector<uint64_t>& lens);
 int plan_tiles(Handle* h, const std::vector<uint64_t>& lens);
 int recode_slots(Handle* h, bool decode);
+int plan_slices(Handle* h, const std::vector<Tile>& tiles, std::vector<Segment>& segs);
+int build_slices(Handle* h);
+int decode_rows(const Handle* h, uint64_t r0, uint64_t r1, uint32_t* d_col, uint16_t* d_val);
+template <typename Acc>
+int launch_slices(Handle* h, const Acc* x, double* y, cudaStream_t s);
+// the upload's row pointer (rows in the reference's order)
+inline const uint64_t* orig_row_ptr(const Handle* h) { return h->d_row_ptr_orig ? h->d_row_ptr_orig : h->d_row_ptr; }
 int grid_for(uint64_t work_items, int threads, int max_blocks_per_sm = 8);
 
 }  // namespace dg

@@ -66,72 +66,6 @@ __global__ void k_split_rows(M mat, const uint64_t* __restrict__ rp,
   }
 }
 
-// ---- slot assignment (replicated x windows, spmv_tiles.cuh) ----------------------------------
-// One half-chunk: the <= 16 positions of a segment that one half-warp gathers in one LDS.64.
-// Each position may read its column from any of the kReplicas replicas (bank pair
-// (c - xlo + shift_r) mod 16); masked-off lanes of a partial half read the filler slot 0 (bank
-// pair 0).  Find the replica choice minimising the largest number of distinct words on one bank
-// pair -- the wavefronts that half costs -- by raising the per-bank capacity L from its lower
-// bound until a b-matching of positions to bank pairs exists (BFS augmenting paths; <= 16 x 3
-// edges).  Deterministic: the same stream and plan always give the same slots.
-struct HalfMatch {
-  uint8_t opt[16][kReplicas];  // bank pair per (position, replica)
-  int8_t asg[16];              // replica chosen per position (-1: none yet)
-  uint8_t load[16];
-  int n;
-
-  __device__ int bank(int i) const { return opt[i][asg[i]]; }
-  // one augmenting path from position s under capacities cap[]; false if none
-  __device__ bool augment(int s, const uint8_t* cap) {
-    int8_t via[16];          // via[b]: position that reached bank pair b
-    uint8_t q[16];
-    uint32_t seen_b = 0, seen_p = 1u << s;
-    int qh = 0, qt = 0;
-    q[qt++] = static_cast<uint8_t>(s);
-    int found = -1;
-    while (qh < qt && found < 0) {
-      const int u = q[qh++];
-      for (int r = 0; r < static_cast<int>(kReplicas) && found < 0; ++r) {
-        const int b = opt[u][r];
-        if ((seen_b >> b) & 1u) continue;
-        seen_b |= 1u << b;
-        via[b] = static_cast<int8_t>(u);
-        if (load[b] < cap[b]) { found = b; break; }
-        for (int v = 0; v < n; ++v)
-          if (asg[v] >= 0 && bank(v) == b && !((seen_p >> v) & 1u)) {
-            seen_p |= 1u << v;
-            q[qt++] = static_cast<uint8_t>(v);
-          }
-      }
-    }
-    if (found < 0) return false;
-    int b = found;
-    for (;;) {  // shift every position on the path one step: only `found` gains a word
-      const int u = via[b];
-      const int prev = asg[u] >= 0 ? bank(u) : -1;
-      for (int r = 0; r < static_cast<int>(kReplicas); ++r)
-        if (opt[u][r] == b) { asg[u] = static_cast<int8_t>(r); break; }
-      if (prev < 0) break;
-      b = prev;
-    }
-    ++load[found];
-    return true;
-  }
-  __device__ void solve(bool filler) {
-    for (int L = (n + 15) / 16 > 0 ? (n + 15) / 16 : 1;; ++L) {
-      uint8_t cap[16];
-      for (int b = 0; b < 16; ++b) {
-        cap[b] = static_cast<uint8_t>(L - (filler && b == 0 ? 1 : 0));
-        load[b] = 0;
-      }
-      for (int i = 0; i < n; ++i) asg[i] = -1;
-      bool ok = true;
-      for (int i = 0; i < n && ok; ++i) ok = augment(i, cap);
-      if (ok) return;
-    }
-  }
-};
-
 // decode == 0: rewrite the column field of every position of every slot-mode tile (nrep > 1)
 // into its slot; decode == 1: back to columns (dg_copy_rows, the scatter comparator).
 // One warp per tile, half-chunks strided over its lanes.
@@ -166,7 +100,7 @@ __global__ void k_assign_slots(uint32_t* __restrict__ w, const Tile* __restrict_
           for (uint32_t r = 0; r < kReplicas; ++r)
             m.opt[i][r] = static_cast<uint8_t>((col[i] - T.xlo + rep_shift(r)) & 15u);
         }
-        m.solve(e - a < 16);
+        m.solve(e - a < 16, 0);
         for (int i = 0; i < m.n; ++i) {
           const uint32_t v = w[base0 + a + i];
           w[base0 + a + i] = (slot_of(col[i], T.xlo, m.asg[i], stride) << 16) | (v & 0xFFFFu);
@@ -188,7 +122,9 @@ template <class M>
 int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens) {
   const uint64_t rows = h->rows;
   const uint32_t align = 16u / h->acc_bytes;                  // elements per 16 B (TMA alignment)
-  const uint32_t W = h->window_cols;                          // window capacity (columns)
+  // slice stream (spmv_slices.cuh): the last element of every window buffer is the zero slot
+  bool slices = h->slices_wanted;
+  const uint32_t W = h->window_cols - (slices ? 16u : 0u);    // window capacity (columns)
   const uint32_t ws = W - align;                              // max segment span
   // narrow bound: sparse segments are kept within A columns so they pack into the fixed grid of
   // windows below (stride W - A); dense rows may span a whole window (their lanes read
@@ -249,7 +185,8 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     }
     dense_all = longest && h->nnz < 200ull * h->sm_count * longest && 20 * dnnz >= h->nnz;
   }
-  h->dense_kernel = h->dense_mode != 0 && (dense_all || 100 * wide_dense >= h->nnz);
+  // (the slice stream has no global-x segments: every dense row wider than a window is k_dense's)
+  h->dense_kernel = h->dense_mode != 0 && (dense_all || 100 * wide_dense >= h->nnz || (slices && wide_dense));
   std::vector<std::vector<HostSeg>> waves(1);
   std::vector<HostSeg> global_x;
   std::vector<uint32_t> wide, dense_rows;
@@ -265,7 +202,7 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
       h->dense_nnz += lens[r];
       continue;
     }
-    const bool dense_long = lens[r] >= h->global_min_len && dense;
+    const bool dense_long = !slices && lens[r] >= h->global_min_len && dense;
     if ((span <= A || (dense && span <= ws)) && !dense_long) {
       waves[0].push_back({rp[r], static_cast<uint32_t>(lens[r]), static_cast<uint32_t>(r), 0, c0,
                           c1, 0, whole});
@@ -351,6 +288,8 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
   // wave.  DG_FUSE_WAVES=0 keeps one launch per wave.
   h->fused_waves = h->n_waves > 1;
   if (const char* fw = std::getenv("DG_FUSE_WAVES")) h->fused_waves = h->fused_waves && std::atoi(fw);
+  if (h->n_waves > 1 && !h->fused_waves) slices = false;  // one launch list only
+  if (!global_x.empty()) slices = false;  // (DG_DENSE=0: global-x tiles need true columns)
   // Output row blocks: contiguous, byte-balanced row ranges.  A block's d is complete (and can be
   // downloaded) once its tiles are done.  Fused waves list the (wave, block) groups diagonally --
   // wave w of block b right after wave w - 1 of block b + lag -- with lag = K - 1 (wave after
@@ -465,7 +404,8 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     auto& S = win[w][k];
     auto cls = [&](const HostSeg& q) -> int {
       const uint32_t span = q.chi - q.clo + 1;
-      if (rep && span <= A3 && 4ull * q.n < 3ull * span) return 0;
+      // (slot mode on the row-ordered stream: Packed16 only -- k_assign_slots rewrites it)
+      if (rep && (slices || h->packed) && span <= A3 && 4ull * q.n < 3ull * span) return 0;
       return narrow(q) ? 1 : 2;
     };
     auto bin = [&](const HostSeg& q, int c) -> uint32_t {
@@ -544,6 +484,8 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     h->fused_rows = lrows[0];
     h->fused_nnz = ldone[0];
   }
+  if (slices) DG_TRY(plan_slices(h, ltiles[0], lsegs[0]));
+  h->n_segments = lsegs[0].size();
   for (uint32_t lw = 0; lw < NL; ++lw) {  // the fused list is uploaded as launch 0
     const auto& tiles = ltiles[lw];
     const auto& segs = lsegs[lw];
@@ -558,7 +500,7 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     h->plan_bytes += tiles.size() * sizeof(Tile) + segs.size() * sizeof(Segment);
     for (const Tile& t : tiles) h->slot_tiles += t.nrep > 1;
   }
-  if (h->slot_tiles) DG_TRY(recode_slots(h, false));
+  if (h->slot_tiles && !h->slices) DG_TRY(recode_slots(h, false));
   if (h->n_carry_slots) {
     const uint64_t n = h->n_carry_slots * 32;
     DG_CUDA(cudaMalloc(&h->d_state, n * h->acc_bytes));
@@ -584,7 +526,7 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
 // Rewrite the slot-mode tiles' positions of the Packed16 stream between columns (decode) and
 // slots (encode); the handle remembers which form the stream is in.
 int recode_slots(Handle* h, bool decode) {
-  if (!h->slot_tiles || h->slots_encoded == !decode) return DG_OK;
+  if (h->slices || !h->slot_tiles || h->slots_encoded == !decode) return DG_OK;
   const uint32_t NL = h->fused_waves ? 1 : h->n_waves;
   for (uint32_t lw = 0; lw < NL; ++lw) {
     if (!h->wave_tiles[lw]) continue;

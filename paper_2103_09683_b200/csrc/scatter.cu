@@ -163,6 +163,22 @@ int dg_scatter_create(const dg_csr_view* v, uint32_t chunk_count, int32_t device
   cu(cudaMalloc(&idx, nz * 4));
   cu(cudaMalloc(&perm, nz * 4));
   if (st == DG_OK) st = dg::recode_slots(h, true);  // columns, not slots (the next dose re-encodes)
+  // a slice-stream handle: the row-ordered encoding decoded into a (u32 column, binary16) view
+  dg::Handle view;
+  uint32_t* v_col = nullptr;
+  uint16_t* v_val = nullptr;
+  if (st == DG_OK && h->slices) {
+    cu(cudaMalloc(&v_col, nz * 4));
+    cu(cudaMalloc(&v_val, nz * 2));
+    if (st == DG_OK) st = dg::decode_rows(h, 0, h->rows, v_col, v_val);
+    view.packed = false;
+    view.value_precision = DG_HALF;
+    view.index_bytes = 4;
+    view.d_col = v_col;
+    view.d_val = v_val;
+    view.d_row_ptr = h->d_row_ptr_orig;
+    h = &view;
+  }
   if (st == DG_OK) {
     cu(cudaMemset(s->d_col_ptr, 0, (s->cols + 1) * 8));
     dg::k_row_of<<<dg::grid_for(s->rows, 256), 256>>>(h->d_row_ptr, s->rows, r_of);
@@ -203,6 +219,10 @@ int dg_scatter_create(const dg_csr_view* v, uint32_t chunk_count, int32_t device
   cudaFree(keys_out);
   cudaFree(idx);
   cudaFree(perm);
+  cudaFree(v_col);
+  cudaFree(v_val);
+  view.d_col = view.d_val = nullptr;
+  view.d_row_ptr = nullptr;
   dg_destroy(hh);
   if (st) {
     dg_scatter_destroy(s);

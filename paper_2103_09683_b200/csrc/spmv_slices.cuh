@@ -1,0 +1,274 @@
+// spmv_slices.cuh -- the tile kernel over the slice stream (warp-contiguous, 128-bit streaming).
+//
+// The slice stream is the binary16 matrix re-laid out once at dg_create for the tile kernel:
+//   * per tile, per warp of the CTA, one contiguous run of 8-chunk batches (the plan assigns the
+//     tile's segments to warps, LPT on chunks), tiles in claim order;
+//   * a chunk is 32 words, one per logical lane of ONE segment: word l of a segment's chunk j is
+//     the nonzero at position base0 + 32 j + l (base0 = the row's lane grid, Segment::lane0), so
+//     lane l still owns the reference's lane l (positions start + l, start + l + 32, ...);
+//     positions outside the segment are neutral words (value +0, the window's zero slot);
+//   * a word is (slot << 16) | binary16 bits: the slot indexes the tile's x-window buffer
+//     directly (column - xlo, or the replica slot of spmv_tiles.cuh) -- 4 bytes per nonzero,
+//     for U32-indexed matrices too;
+//   * 4 consecutive chunks form one 512-byte block stored lane-major (word 4 l + k = chunk k,
+//     lane l), so each lane fetches its next 4 chunk words with one 16-byte load: a batch of
+//     8 chunks is two fully coalesced LDG.128 per lane, aligned to 128-byte lines.
+// Compared with the row-ordered stream (k_tiles): no segment-edge lines fetched twice (adjacent
+// rows of the row-ordered stream sit in unrelated tiles), no misaligned 2-line chunk requests, no
+// masked edge batches; the price is the neutral padding (< 32 words per segment end, < 8 chunks
+// per warp range).  Results are bit-identical: each lane adds the same products in the same
+// order from +0.0, and a neutral word adds +0 * (+0.0) = +0.0, the identity of an accumulator
+// that is never -0.0.
+#pragma once
+
+#include "common.cuh"
+#include "spmv_kernels.cuh"
+#include "spmv_tiles.cuh"
+
+namespace dg {
+
+// per (tile, warp): first chunk and first segment of the warp's run; entry t * WARPS + w, with one
+// sentinel at the end (runs are contiguous in tile order)
+struct WarpRange {
+  uint32_t chunk;
+  uint32_t seg;
+};
+// the kernel's segment descriptor (16 bytes, one LDG.128)
+struct SliceSeg {
+  uint32_t row;
+  uint32_t slot;   // carried-partials slot (split rows)
+  uint32_t nch;    // chunks
+  uint32_t flags;  // kSegFirst | kSegLast
+};
+
+constexpr int kSliceU = 8;  // chunks per batch (two 512-byte blocks)
+
+__device__ __forceinline__ uint4 ld_stream16(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.cs.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+// One warp's run: nb batches starting at chunk c0.  Software pipeline: batch b + 1 is in flight
+// in registers while batch b is gathered and accumulated; lanes 0..7 prefetch the 8 lines of
+// batch b + 1 + P into L2.
+template <typename Acc, int P, bool CARRY>
+__device__ __forceinline__ void run_slice(const uint4* __restrict__ blocks, uint32_t c0, uint32_t nb,
+                                          const SliceSeg* __restrict__ sseg, uint32_t s0,
+                                          uint32_t s1, const Acc* xs, const Carry<Acc>& carry,
+                                          double* __restrict__ y, const GatherTargets& gt,
+                                          uint32_t lane) {
+  using Ops = AccOps<Acc>;
+  if (nb == 0) return;
+  // current segment and the next one's descriptor (loaded one segment ahead)
+  uint32_t si = s0;
+  SliceSeg cur = sseg[si];
+  SliceSeg nxt = si + 1 < s1 ? sseg[si + 1] : SliceSeg{0, 0, 0, 0};
+  uint32_t left = cur.nch;
+  Acc acc = CARRY ? carry.in(cur.slot, cur.flags, lane) : Acc(0);
+  const uint4* p = blocks + static_cast<uint64_t>(c0 / 4) * 32 + lane;  // block c0/4, lane's 16 B
+  uint4 a0 = ld_stream16(p), a1 = ld_stream16(p + 32), b0, b1;
+  if constexpr (P > 0) {
+#pragma unroll
+    for (int k = 1; k <= P; ++k)
+      if (lane < 8 && static_cast<uint32_t>(k) < nb)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(p - lane + 64 * k) + 128 * lane));
+  }
+  auto finish = [&]() {  // the current segment ends with the chunk just added
+    if (!CARRY || (cur.flags & kSegLast)) {
+#pragma unroll
+      for (int off = 16; off >= 1; off /= 2) acc = Ops::add(acc, __shfl_down_sync(kFull, acc, off));
+      if (lane == 0) {
+        y[cur.row] = static_cast<double>(acc);
+        gt.store(cur.row, static_cast<double>(acc));
+      }
+    } else {
+      if constexpr (CARRY) carry.out(cur.slot, cur.flags, lane, acc);
+    }
+    ++si;
+    if (si < s1) {
+      cur = nxt;
+      left = cur.nch;
+      acc = CARRY ? carry.in(cur.slot, cur.flags, lane) : Acc(0);
+      if (si + 1 < s1) nxt = sseg[si + 1];
+    } else {
+      left = 0xFFFFFFFFu;  // the run's padding chunks: neutral words, no segment
+      acc = Acc(0);
+    }
+  };
+  auto consume = [&](const uint4& q0, const uint4& q1) {
+    const uint32_t r[kSliceU] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+    Acc xv[kSliceU];
+#pragma unroll
+    for (int k = 0; k < kSliceU; ++k) xv[k] = xs[r[k] >> 16];
+    if (left > static_cast<uint32_t>(kSliceU)) {  // the whole batch inside one segment
+#pragma unroll
+      for (int k = 0; k < kSliceU; ++k)
+        acc = Ops::add(acc, Ops::prod(static_cast<uint16_t>(r[k] & 0xFFFFu), xv[k]));
+      left -= kSliceU;
+      return;
+    }
+#pragma unroll
+    for (int k = 0; k < kSliceU; ++k) {
+      acc = Ops::add(acc, Ops::prod(static_cast<uint16_t>(r[k] & 0xFFFFu), xv[k]));
+      if (--left == 0) finish();
+    }
+  };
+  uint32_t bi = 0;
+  for (;;) {
+    // step A: consume a, load b
+    if (bi + 1 < nb) {
+      b0 = ld_stream16(p + 64);
+      b1 = ld_stream16(p + 96);
+    }
+    if constexpr (P > 0)
+      if (lane < 8 && bi + 1 + P < nb)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(p - lane + 64 * (1 + P)) + 128 * lane));
+    consume(a0, a1);
+    if (++bi == nb) break;
+    p += 64;
+    // step B: consume b, load a
+    if (bi + 1 < nb) {
+      a0 = ld_stream16(p + 64);
+      a1 = ld_stream16(p + 96);
+    }
+    if constexpr (P > 0)
+      if (lane < 8 && bi + 1 + P < nb)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(p - lane + 64 * (1 + P)) + 128 * lane));
+    consume(b0, b1);
+    if (++bi == nb) break;
+    p += 64;
+  }
+}
+
+// Persistent: one CTA per SM, NB x-window buffers of wcap elements (dynamic smem), element
+// wcap - 1 of each buffer is the zero slot the neutral words gather.
+template <typename Acc, int WARPS, int P, bool CARRY, int NB = 2>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+    k_slices(const uint4* __restrict__ blocks, XSource<Acc> xsrc, const Tile* __restrict__ tiles,
+             uint32_t n_tiles, const WarpRange* __restrict__ ranges,
+             const SliceSeg* __restrict__ sseg, Carry<Acc> carry, double* __restrict__ y,
+             uint32_t* __restrict__ counter, uint32_t wcap, BlockSignal sig,
+             const __grid_constant__ GatherTargets gt, TileTrace tr) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[NB];
+  __shared__ uint32_t tile_of[NB], done[NB];
+  Acc* const xbuf0 = reinterpret_cast<Acc*>(smem_raw);
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const Acc* __restrict__ x = xsrc.x;
+
+  auto refill = [&](int b) {
+    const uint32_t t = atomicAdd(counter, 1u);
+    tile_of[b] = t;
+    done[b] = 0;
+    if (t < n_tiles) {
+      const Tile T = tiles[t];
+      if (tr.cta) {
+        tr.tile[3ull * t] = gtimer_ns();
+        tr.tile[3ull * t + 2] = blockIdx.x | (static_cast<unsigned long long>(T.seg1 - T.seg0) << 16);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      char* const dst0 = reinterpret_cast<char*>(xbuf0 + b * wcap);
+      constexpr uint32_t kAl = 16 / sizeof(Acc);
+      uint32_t total = 0;
+      const uint32_t nrep = T.nrep;
+      for (uint32_t r = 0; r < nrep; ++r)
+        total += (T.xlen + rep_shift(r) + kAl - 1) / kAl * kAl * static_cast<uint32_t>(sizeof(Acc));
+      mbar_arrive_expect_tx(&full[b], total);
+      for (uint32_t r = 0; r < nrep; ++r) {
+        const uint32_t sh = rep_shift(r);
+        const uint32_t bytes = (T.xlen + sh + kAl - 1) / kAl * kAl * static_cast<uint32_t>(sizeof(Acc));
+        const Acc* base = (sh % kAl) ? xsrc.x1 : x;
+        const char* src = reinterpret_cast<const char*>(base + T.xlo) - sh * sizeof(Acc);
+        char* dst = dst0 + static_cast<size_t>(r) * xsrc.rep_stride * sizeof(Acc);
+        for (uint32_t off = 0; off < bytes; off += 32768u)
+          tma_load_1d(dst + off, src + off, min(32768u, bytes - off), &full[b]);
+      }
+      // the first 2 KB of every warp's run and the tile's segment descriptors into L2: the
+      // warps start the tile on L2 hits
+      const WarpRange* R = ranges + static_cast<uint64_t>(t) * WARPS;
+      for (int w = 0; w < WARPS; ++w) {
+        const uint32_t c = R[w].chunk, ce = R[w + 1].chunk;
+        if (ce > c)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(blocks + static_cast<uint64_t>(c / 4) * 32),
+                       "r"(min(2048u, (ce - c) * 128u))
+                       : "memory");
+      }
+      const uint64_t sb = reinterpret_cast<uint64_t>(sseg + R[0].seg) & ~15ull;
+      const uint64_t se = reinterpret_cast<uint64_t>(sseg + R[WARPS].seg);
+      if (se > sb)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sb),
+                     "r"(static_cast<uint32_t>(se - sb))
+                     : "memory");
+    } else {
+      mbar_arrive(&full[b]);
+    }
+  };
+
+  if (threadIdx.x < NB) xbuf0[threadIdx.x * wcap + wcap - 1] = Acc(0);  // zero slots
+  if (threadIdx.x == 0)
+    for (int i = 0; i < NB; ++i) mbar_init(&full[i], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int i = 0; i < NB; ++i) refill(i);
+  __syncthreads();
+
+  uint32_t phases = 0;
+  int b = 0;
+  const long long clk0 = clock64();
+  long long wait_cyc = 0;
+  if (tr.cta && threadIdx.x == 0) tr.cta[4ull * blockIdx.x] = gtimer_ns();
+  for (;;) {
+    if (tr.cta) {
+      const long long w0 = clock64();
+      mbar_wait(&full[b], (phases >> b) & 1u);
+      wait_cyc += clock64() - w0;
+    } else {
+      mbar_wait(&full[b], (phases >> b) & 1u);
+    }
+    phases ^= 1u << b;
+    const uint32_t t = *reinterpret_cast<volatile uint32_t*>(&tile_of[b]);
+    if (t >= n_tiles) break;
+    const WarpRange r0 = ranges[static_cast<uint64_t>(t) * WARPS + warp];
+    const WarpRange r1 = ranges[static_cast<uint64_t>(t) * WARPS + warp + 1];
+    run_slice<Acc, P, CARRY>(blocks, r0.chunk, (r1.chunk - r0.chunk) / kSliceU, sseg, r0.seg, r1.seg,
+                             xbuf0 + b * wcap, carry, y, gt, lane);
+    __syncwarp();
+    if (lane == 0) {
+      if (sig.left) __threadfence(); else __threadfence_block();
+      if (atomicAdd(&done[b], 1u) == WARPS - 1) {
+        __threadfence_block();
+        const Tile T = tiles[t];
+        if (tr.cta) tr.tile[3ull * t + 1] = gtimer_ns();
+        if (sig.left && T.blk != kNoBlock) {
+          __threadfence();
+          if (atomicSub(&sig.left[T.blk], 1u) == 1u) {
+            __threadfence();
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(sig.flag + T.blk),
+                         "r"(sig.epoch)
+                         : "memory");
+          }
+        }
+        refill(b);
+      }
+    }
+    __syncwarp();
+    b = b + 1 == NB ? 0 : b + 1;
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (tr.cta && lane == 0) {
+    atomicAdd(&tr.cta[4ull * blockIdx.x + 2], static_cast<unsigned long long>(wait_cyc));
+    atomicAdd(&tr.cta[4ull * blockIdx.x + 3], static_cast<unsigned long long>(clock64() - clk0));
+    atomicMax(&tr.cta[4ull * blockIdx.x + 1], gtimer_ns());
+  }
+}
+
+// word index of (chunk c, lane l) in the lane-major 4-chunk blocks
+__host__ __device__ __forceinline__ uint64_t slice_word(uint64_t c, uint32_t l) {
+  return (c >> 2) * 128 + 4 * l + (c & 3);
+}
+
+}  // namespace dg

@@ -207,6 +207,72 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       : "memory");
 }
 
+// ---- slot assignment ---------------------------------------------------------------------------
+// One half-chunk: the <= 16 positions of a segment that one half-warp gathers in one LDS.64.
+// Each position may read its column from any of the kReplicas replicas (bank pair
+// (c - xlo + shift_r) mod 16); masked-off lanes of a partial half read one filler slot (bank
+// pair fb).  Find the replica choice minimising the largest number of distinct words on one bank
+// pair -- the wavefronts that half costs -- by raising the per-bank capacity L from its lower
+// bound until a b-matching of positions to bank pairs exists (BFS augmenting paths; <= 16 x 3
+// edges).  Deterministic: the same stream and plan always give the same slots.
+struct HalfMatch {
+  uint8_t opt[16][kReplicas];  // bank pair per (position, replica)
+  int8_t asg[16];              // replica chosen per position (-1: none yet)
+  uint8_t load[16];
+  int n;
+
+  __device__ int bank(int i) const { return opt[i][asg[i]]; }
+  // one augmenting path from position s under capacities cap[]; false if none
+  __device__ bool augment(int s, const uint8_t* cap) {
+    int8_t via[16];          // via[b]: position that reached bank pair b
+    uint8_t q[16];
+    uint32_t seen_b = 0, seen_p = 1u << s;
+    int qh = 0, qt = 0;
+    q[qt++] = static_cast<uint8_t>(s);
+    int found = -1;
+    while (qh < qt && found < 0) {
+      const int u = q[qh++];
+      for (int r = 0; r < static_cast<int>(kReplicas) && found < 0; ++r) {
+        const int b = opt[u][r];
+        if ((seen_b >> b) & 1u) continue;
+        seen_b |= 1u << b;
+        via[b] = static_cast<int8_t>(u);
+        if (load[b] < cap[b]) { found = b; break; }
+        for (int v = 0; v < n; ++v)
+          if (asg[v] >= 0 && bank(v) == b && !((seen_p >> v) & 1u)) {
+            seen_p |= 1u << v;
+            q[qt++] = static_cast<uint8_t>(v);
+          }
+      }
+    }
+    if (found < 0) return false;
+    int b = found;
+    for (;;) {  // shift every position on the path one step: only `found` gains a word
+      const int u = via[b];
+      const int prev = asg[u] >= 0 ? bank(u) : -1;
+      for (int r = 0; r < static_cast<int>(kReplicas); ++r)
+        if (opt[u][r] == b) { asg[u] = static_cast<int8_t>(r); break; }
+      if (prev < 0) break;
+      b = prev;
+    }
+    ++load[found];
+    return true;
+  }
+  __device__ void solve(bool filler, int fb) {
+    for (int L = (n + 15) / 16 > 0 ? (n + 15) / 16 : 1;; ++L) {
+      uint8_t cap[16];
+      for (int b = 0; b < 16; ++b) {
+        cap[b] = static_cast<uint8_t>(L - (filler && b == fb ? 1 : 0));
+        load[b] = 0;
+      }
+      for (int i = 0; i < n; ++i) asg[i] = -1;
+      bool ok = true;
+      for (int i = 0; i < n && ok; ++i) ok = augment(i, cap);
+      if (ok) return;
+    }
+  }
+};
+
 // x sources: the tile's shared-memory window, or global x (L1/L2) for dense wide rows whose
 // column span exceeds a window (kSegGlobalX) -- their 32 lanes read 32 consecutive x entries.
 // The window is indexed by the stream's 16-bit field directly: `base` is the buffer minus xlo in
