@@ -12,7 +12,8 @@
  *   dg_dose            <- ddm::spmv_rowchunk(const CsrMatrix&, const DenseVector&,
  *                         const RowChunkConfig&)  (include/ddm/spmv.hpp:37, src/spmv.cpp:98-111)
  *                         and, with lane_width 1, ddm::spmv_oracle (spmv.hpp:29, spmv.cpp:82-96).
- *   dg_checksum_bits   <- ddm::checksum_bits (include/ddm/checksum.hpp:25-35), computed on device.
+ *   dg_checksum_bits   <- ddm::checksum_bits (include/ddm/checksum.hpp:25-35).  FNV-1a is a
+ *                         sequential hash: a device array is copied to the host and hashed there.
  *   dg_traffic_bytes   <- ddm::traffic(dims_of(m), layout_of(m)).total_bytes()
  *                         (src/perf_model.cpp:41-54) -- the algorithmic bytes of one evaluation.
  *   dg_partition_rows  <- replaces parallel_blocks' equal-row-count split (src/spmv.cpp:17-32)
@@ -27,7 +28,8 @@
  *
  * Ownership: the caller owns every array it passes; dg_create copies what it needs to the device
  * and keeps no host pointer.  The handle owns all device memory.  Threading: one host thread per
- * handle at a time; handles are independent; the matrix is immutable after dg_create.
+ * handle at a time; handles are independent; the matrix is immutable after dg_create.  Every
+ * entry point restores the calling thread's current CUDA device before it returns.
  */
 #ifndef DOSEGPU_H
 #define DOSEGPU_H
@@ -125,6 +127,8 @@ int dg_generated_row_lengths(const dg_profile* beams, uint32_t n_beams, uint64_t
                              uint64_t row_end, int32_t device, uint32_t* lengths_out);
 
 /* DDM1 file -> device, streamed (ddm::read_ddm, src/io.cpp:103-168; format io.hpp:10-20).
+ * With opts->row_begin / row_end only that shard's byte ranges of the column and value sections
+ * are read (pread at the offsets the header fixes): device memory holds the shard, not the file.
  * The header is checked exactly as the reference does (BadMagic, UnsupportedVersion,
  * ValidationFailure for bad precision/index/reserved bytes or implausible sizes, TruncatedFile,
  * ValidationFailure for trailing bytes), row pointers are read to the host, and the column and
@@ -227,7 +231,8 @@ int dg_copy_rows(const dg_handle* h, uint64_t r0, uint64_t r1, uint64_t* row_ptr
 /* Row pointers [r0, r1] of the shard (r1 - r0 + 1 entries, shard-relative, NOT rebased). */
 int dg_copy_row_ptr(const dg_handle* h, uint64_t r0, uint64_t r1, uint64_t* row_ptr_out);
 
-/* FNV-1a-64 over the bit patterns of a device or host double array (checksum.hpp:25-35). */
+/* FNV-1a-64 over the bit patterns of a device or host double array (checksum.hpp:25-35); a
+ * device array is copied to the host first (the hash is sequential). */
 int dg_checksum_bits(const double* v, uint64_t n, int on_device, uint64_t* out);
 
 /* Algorithmic bytes of one evaluation (perf_model.cpp:41-54 with layout_of: row_ptr 8 B and

@@ -117,6 +117,23 @@ struct GatherTargets {
   }
 };
 
+// Host side: every dg_* entry point that selects a device restores the caller's current device
+// when it returns (a host thread driving several GPUs keeps its own device selection).
+struct DeviceGuard {
+  int prev = -1;
+  DeviceGuard() {
+    if (cudaGetDevice(&prev) != cudaSuccess) {
+      prev = -1;
+      cudaGetLastError();
+    }
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 __device__ __forceinline__ uint32_t pack16(uint16_t col, uint16_t half_bits) {
   return (static_cast<uint32_t>(col) << 16) | half_bits;
 }

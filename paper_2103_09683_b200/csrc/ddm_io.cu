@@ -6,6 +6,13 @@
 // here the column and value sections are read with large pread()s into two pinned buffers and
 // copied asynchronously to the device while the next chunk is read; dg_create then validates,
 // packs and plans the device copy.
+//
+// Row shards (opts->row_begin / row_end): the section layout is fixed by the header (io.cpp:67-96,
+// 103-168), so a rank reads the whole row_ptr section (8 B per row: every row_ptr invariant is
+// checked, as read_ddm does) but only the byte ranges [rp[r0], rp[r1]) of the column and value
+// sections -- peak device memory is the shard, not the file.  The per-entry invariants
+// (ddm::validate: columns in range and increasing, finite values) are checked on the shard's
+// entries.
 #include <cuda_runtime.h>
 #include <fcntl.h>
 #include <sys/stat.h>
@@ -62,7 +69,9 @@ int stream_section(int fd, off_t off, uint64_t bytes, char* d_dst, char* pinned[
 }  // namespace
 
 extern "C" int dg_create_from_ddm(const char* path, const dg_options* opts, dg_handle** out) {
+  dg::DeviceGuard device_guard;  // the caller's current device is restored on return
   if (!path || !out) return DG_ERR_INVALID_CONFIG;
+  if (opts) DG_TRY(dg::check_options(opts));
   *out = nullptr;
   Fd f;
   f.fd = open(path, O_RDONLY);
@@ -98,8 +107,18 @@ extern "C" int dg_create_from_ddm(const char* path, const dg_options* opts, dg_h
   std::vector<uint64_t> rp(rows + 1);
   if (!read_all(f.fd, rp.data(), 8 * (rows + 1), static_cast<off_t>(rp_off)))
     return DG_ERR_TRUNCATED_FILE;
+  // row_ptr invariants of the whole file (sparse.cpp:221-229)
+  if (rp[0] != 0 || rp[rows] != nnz) return DG_ERR_VALIDATION_FAILURE;
+  for (uint64_t r = 0; r < rows; ++r)
+    if (rp[r + 1] < rp[r]) return DG_ERR_VALIDATION_FAILURE;
+  const uint64_t r0 = opts ? opts->row_begin : 0;
+  const uint64_t r1 = opts && opts->row_end ? opts->row_end : rows;
+  if (r0 > r1 || r1 > rows) return DG_ERR_INVALID_CONFIG;
+  const uint64_t n_rows = r1 - r0, p0 = rp[r0], snnz = rp[r1] - rp[r0];
+  std::vector<uint64_t> srp(n_rows + 1);
+  for (uint64_t r = 0; r <= n_rows; ++r) srp[r] = rp[r0 + r] - p0;
 
-  // device staging of the three sections, then the regular create path on a device view
+  // device staging of the shard's three sections, then the regular create path on a device view
   uint64_t* d_rp = nullptr;
   char *d_col = nullptr, *d_val = nullptr, *pinned[2] = {nullptr, nullptr};
   cudaStream_t s = nullptr;
@@ -107,9 +126,9 @@ extern "C" int dg_create_from_ddm(const char* path, const dg_options* opts, dg_h
   const size_t chunk = 64ull << 20;
   int rc = DG_OK;
   auto cu = [&](cudaError_t e) { if (rc == DG_OK && e != cudaSuccess) rc = DG_ERR_CUDA_BASE + (int)e; };
-  cu(cudaMalloc(&d_rp, 8 * (rows + 1)));
-  cu(cudaMalloc(&d_col, std::max<uint64_t>(ib * nnz, 16)));
-  cu(cudaMalloc(&d_val, std::max<uint64_t>(vb * nnz, 16)));
+  cu(cudaMalloc(&d_rp, 8 * (n_rows + 1)));
+  cu(cudaMalloc(&d_col, std::max<uint64_t>(ib * snnz, 16)));
+  cu(cudaMalloc(&d_val, std::max<uint64_t>(vb * snnz, 16)));
   cu(cudaHostAlloc(&pinned[0], chunk, cudaHostAllocDefault));
   cu(cudaHostAlloc(&pinned[1], chunk, cudaHostAllocDefault));
   cu(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -118,16 +137,18 @@ extern "C" int dg_create_from_ddm(const char* path, const dg_options* opts, dg_h
   if (rc == DG_OK) {
     cu(cudaEventRecord(done[0], s));
     cu(cudaEventRecord(done[1], s));
-    cu(cudaMemcpyAsync(d_rp, rp.data(), 8 * (rows + 1), cudaMemcpyHostToDevice, s));
+    cu(cudaMemcpyAsync(d_rp, srp.data(), 8 * (n_rows + 1), cudaMemcpyHostToDevice, s));
   }
-  if (rc == DG_OK) rc = stream_section(f.fd, static_cast<off_t>(col_off), ib * nnz, d_col, pinned, chunk, s, done);
-  if (rc == DG_OK) rc = stream_section(f.fd, static_cast<off_t>(val_off), vb * nnz, d_val, pinned, chunk, s, done);
+  if (rc == DG_OK)
+    rc = stream_section(f.fd, static_cast<off_t>(col_off + ib * p0), ib * snnz, d_col, pinned, chunk, s, done);
+  if (rc == DG_OK)
+    rc = stream_section(f.fd, static_cast<off_t>(val_off + vb * p0), vb * snnz, d_val, pinned, chunk, s, done);
   if (rc == DG_OK) cu(cudaStreamSynchronize(s));
   if (rc == DG_OK) {
     dg_csr_view v{};
-    v.rows = rows;
+    v.rows = n_rows;
     v.cols = cols;
-    v.nnz = nnz;
+    v.nnz = snnz;
     v.value_precision = h[5];
     v.index_bytes = static_cast<uint8_t>(ib);
     v.col_storage_bytes = static_cast<uint8_t>(ib);
@@ -139,7 +160,10 @@ extern "C" int dg_create_from_ddm(const char* path, const dg_options* opts, dg_h
     dg_default_options(&o);
     if (opts) o = *opts;
     o.device = dev;
+    o.row_begin = 0;
+    o.row_end = 0;
     rc = dg_create(&v, &o, out);
+    if (rc == DG_OK) dg::set_shard_rows(reinterpret_cast<dg::Handle*>(*out), r0, r1);
   }
   if (s) cudaStreamSynchronize(s);
   cudaFree(d_rp);

@@ -90,9 +90,18 @@ __global__ void k_rebase(uint64_t* __restrict__ rp, uint64_t n, uint64_t base) {
 }
 
 int grid_for(uint64_t work_items, int threads, int max_blocks_per_sm) {
+  // SM count per device, queried once (not on every launch)
+  constexpr int kMaxDev = 64;
+  static int sm_of[kMaxDev] = {};
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (dev >= 0 && dev < kMaxDev) {
+    if (!sm_of[dev]) {
+      int v = 0;
+      if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0) sm_of[dev] = v;
+    }
+    if (sm_of[dev]) sms = sm_of[dev];
+  }
   const uint64_t need = (work_items + threads - 1) / threads;
   const uint64_t cap = static_cast<uint64_t>(sms) * max_blocks_per_sm;
   return static_cast<int>(std::max<uint64_t>(1, std::min(need, cap)));
@@ -491,7 +500,9 @@ int finish_create(Handle* h, const std::vector<uint64_t>& lens) {
   DG_CUDA(cudaEventCreateWithFlags(&h->ev_tiles_start, cudaEventDisableTiming));
   DG_CUDA(cudaEventCreateWithFlags(&h->ev_d2h_done, cudaEventDisableTiming));
   DG_CUDA(cudaStreamCreateWithFlags(&h->d2h_stream, cudaStreamNonBlocking));
-
+  // create-time work (memsets, plan uploads, setup kernels) ran on the legacy stream, which the
+  // handle's non-blocking dose streams do not wait on: finish it before the handle is returned
+  DG_CUDA(cudaDeviceSynchronize());
   return DG_OK;
 }
 
@@ -517,6 +528,7 @@ using dg::Handle;
 extern "C" {
 
 int dg_create(const dg_csr_view* v, const dg_options* opts_in, dg_handle** out) {
+  dg::DeviceGuard device_guard;  // the caller's current device is restored on return
   if (!v || !out) return DG_ERR_INVALID_CONFIG;
   *out = nullptr;
   dg_options opts;
@@ -641,6 +653,7 @@ int dg_create(const dg_csr_view* v, const dg_options* opts_in, dg_handle** out) 
 }
 
 int dg_destroy(dg_handle* hh) {
+  dg::DeviceGuard device_guard;  // the caller's current device is restored on return
   Handle* h = reinterpret_cast<Handle*>(hh);
   if (!h) return DG_OK;
   cudaSetDevice(h->device);
@@ -689,6 +702,7 @@ int dg_destroy(dg_handle* hh) {
 
 int dg_dose(dg_handle* hh, const double* x, uint64_t x_len, double* y, uint32_t flags,
             void* stream) {
+  dg::DeviceGuard device_guard;  // the caller's current device is restored on return
   Handle* h = reinterpret_cast<Handle*>(hh);
   if (!h || (!x && h->cols) || (!y && h->rows)) return DG_ERR_INVALID_CONFIG;
   if (x_len != h->cols) return DG_ERR_DIMENSION_MISMATCH;  // spmv.cpp:34-38
@@ -776,6 +790,7 @@ int dg_get_info(const dg_handle* hh, dg_info* info) {
 }
 
 int dg_last_timing(const dg_handle* hh, dg_timing* t) {
+  dg::DeviceGuard device_guard;  // the caller's current device is restored on return
   Handle* h = const_cast<Handle*>(reinterpret_cast<const Handle*>(hh));
   if (!h || !t) return DG_ERR_INVALID_CONFIG;
   if (!h->timing_valid) {
@@ -788,6 +803,7 @@ int dg_last_timing(const dg_handle* hh, dg_timing* t) {
 }
 
 int dg_kernel_times(const dg_handle* hh, dg_kernel_time* out, uint32_t cap, uint32_t* n_out) {
+  dg::DeviceGuard device_guard;  // the caller's current device is restored on return
   Handle* h = const_cast<Handle*>(reinterpret_cast<const Handle*>(hh));
   if (!h || !n_out) return DG_ERR_INVALID_CONFIG;
   *n_out = 0;
@@ -811,6 +827,7 @@ int dg_kernel_times(const dg_handle* hh, dg_kernel_time* out, uint32_t cap, uint
 }
 
 int dg_debug_trace(const dg_handle* hh, uint64_t* out, uint64_t cap, uint64_t* n_out) {
+  dg::DeviceGuard device_guard;  // the caller's current device is restored on return
   const Handle* h = reinterpret_cast<const Handle*>(hh);
   if (!h || !n_out) return DG_ERR_INVALID_CONFIG;
   *n_out = 0;
@@ -823,6 +840,7 @@ int dg_debug_trace(const dg_handle* hh, uint64_t* out, uint64_t cap, uint64_t* n
 }
 
 int dg_copy_row_ptr(const dg_handle* hh, uint64_t r0, uint64_t r1, uint64_t* rp_out) {
+  dg::DeviceGuard device_guard;  // the caller's current device is restored on return
   const Handle* h = reinterpret_cast<const Handle*>(hh);
   if (!h || !rp_out || r0 > r1 || r1 > h->rows) return DG_ERR_INVALID_CONFIG;
   DG_CUDA(cudaSetDevice(h->device));
@@ -832,6 +850,7 @@ int dg_copy_row_ptr(const dg_handle* hh, uint64_t r0, uint64_t r1, uint64_t* rp_
 
 int dg_copy_rows(const dg_handle* hh, uint64_t r0, uint64_t r1, uint64_t* rp_out,
                  uint32_t* col_out, void* val_out) {
+  dg::DeviceGuard device_guard;  // the caller's current device is restored on return
   const Handle* h = reinterpret_cast<const Handle*>(hh);
   if (!h || r0 > r1 || r1 > h->rows) return DG_ERR_INVALID_CONFIG;
   DG_CUDA(cudaSetDevice(h->device));
@@ -877,6 +896,7 @@ int dg_copy_rows(const dg_handle* hh, uint64_t r0, uint64_t r1, uint64_t* rp_out
 }
 
 int dg_checksum_bits(const double* v, uint64_t n, int on_device, uint64_t* out) {
+  dg::DeviceGuard device_guard;  // the caller's current device is restored on return
   std::vector<double> host;
   const double* p = v;
   if (on_device) {

@@ -16,6 +16,7 @@
 extern "C" {
 
 int dg_set_gather_targets(dg_handle* hh, double* const* targets, uint32_t n) {
+  dg::DeviceGuard device_guard;  // the caller's current device is restored on return
   dg::Handle* h = reinterpret_cast<dg::Handle*>(hh);
   if (!h) return DG_ERR_INVALID_CONFIG;
   if (n > dg::kMaxGatherTargets || (n && !targets)) return DG_ERR_INVALID_CONFIG;
@@ -31,6 +32,7 @@ int dg_set_gather_targets(dg_handle* hh, double* const* targets, uint32_t n) {
 }
 
 int dg_ipc_alloc(uint64_t bytes, int32_t device, void** dptr, void* handle64) {
+  dg::DeviceGuard device_guard;  // the caller's current device is restored on return
   if (!dptr || !handle64) return DG_ERR_INVALID_CONFIG;
   int dev = 0;
   DG_TRY(dg::select_device(device, &dev));
@@ -48,6 +50,7 @@ int dg_ipc_alloc(uint64_t bytes, int32_t device, void** dptr, void* handle64) {
 }
 
 int dg_ipc_open(const void* handle64, int32_t device, void** dptr) {
+  dg::DeviceGuard device_guard;  // the caller's current device is restored on return
   if (!handle64 || !dptr) return DG_ERR_INVALID_CONFIG;
   int dev = 0;
   DG_TRY(dg::select_device(device, &dev));
@@ -58,11 +61,13 @@ int dg_ipc_open(const void* handle64, int32_t device, void** dptr) {
 }
 
 int dg_ipc_close(void* dptr) {
+  dg::DeviceGuard device_guard;  // the caller's current device is restored on return
   DG_CUDA(cudaIpcCloseMemHandle(dptr));
   return DG_OK;
 }
 
 int dg_ipc_free(void* dptr) {
+  dg::DeviceGuard device_guard;  // the caller's current device is restored on return
   DG_CUDA(cudaFree(dptr));
   return DG_OK;
 }

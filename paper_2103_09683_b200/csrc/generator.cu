@@ -182,6 +182,7 @@ extern "C" {
 
 int dg_generated_row_lengths(const dg_profile* p, uint32_t n_beams, uint64_t r0, uint64_t r1,
                              int32_t device, uint32_t* lengths_out) {
+  dg::DeviceGuard device_guard;  // the caller's current device is restored on return
   dg::Beams beams;
   uint64_t rows = 0, cols = 0;
   DG_TRY(dg::to_beams(p, n_beams, &beams, &rows, &cols));
@@ -201,6 +202,7 @@ int dg_generated_row_lengths(const dg_profile* p, uint32_t n_beams, uint64_t r0,
 
 int dg_create_generated(const dg_profile* p, uint32_t n_beams, uint32_t index_bytes,
                         const dg_options* opts_in, dg_handle** out) {
+  dg::DeviceGuard device_guard;  // the caller's current device is restored on return
   if (!out) return DG_ERR_INVALID_CONFIG;
   *out = nullptr;
   dg_options opts;

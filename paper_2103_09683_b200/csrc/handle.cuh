@@ -220,5 +220,10 @@ int launch_slices(Handle* h, const Acc* x, double* y, cudaStream_t s);
 // the upload's row pointer (rows in the reference's order)
 inline const uint64_t* orig_row_ptr(const Handle* h) { return h->d_row_ptr_orig ? h->d_row_ptr_orig : h->d_row_ptr; }
 int grid_for(uint64_t work_items, int threads, int max_blocks_per_sm = 8);
+// a handle created from a shard-only view: record the shard's place in the source matrix
+inline void set_shard_rows(Handle* h, uint64_t r0, uint64_t r1) {
+  h->row_begin = r0;
+  h->row_end = r1;
+}
 
 }  // namespace dg

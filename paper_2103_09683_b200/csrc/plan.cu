@@ -136,7 +136,10 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
   // <= A3 columns (C2: every sparse row, whose columns lie in a 4,096-column locality window),
   // binned on a grid of stride W3 - A3.
   const bool rep = h->slot_mode;
-  const uint32_t RS = W / kReplicas;
+  // (RS a multiple of 16 elements: replica r's bank pairs are then (c - xlo + shift_r) mod 16, the
+  //  model the slot assignment optimises -- with the slice stream's W = 13,808, W / 3 = 4,602 would
+  //  offset replicas 1 and 2 by 10 and 4 bank pairs and the matching would optimise the wrong banks)
+  const uint32_t RS = W / kReplicas / 16 * 16;
   const uint32_t W3 = (RS - 16) / 16 * 16;
   const uint32_t A3 = W3 >= 4096u + 256u ? 4096u : W3 * 2 / 3 / align * align;
   const uint32_t St3 = W3 - A3;

@@ -107,6 +107,7 @@ __global__ void k_merge(const double* __restrict__ scratch, uint64_t rows, uint3
 extern "C" {
 
 int dg_scatter_destroy(dg_scatter* s) {
+  dg::DeviceGuard device_guard;  // the caller's current device is restored on return
   if (!s) return DG_OK;
   cudaSetDevice(s->device);
   if (s->stream) cudaStreamSynchronize(s->stream);
@@ -122,6 +123,7 @@ int dg_scatter_destroy(dg_scatter* s) {
 }
 
 int dg_scatter_create(const dg_csr_view* v, uint32_t chunk_count, int32_t device, dg_scatter** out) {
+  dg::DeviceGuard device_guard;  // the caller's current device is restored on return
   if (!v || !out) return DG_ERR_INVALID_CONFIG;
   *out = nullptr;
   if (chunk_count < 1) return DG_ERR_INVALID_CONFIG;  // spmv.cpp:116
@@ -234,6 +236,7 @@ int dg_scatter_create(const dg_csr_view* v, uint32_t chunk_count, int32_t device
 
 int dg_scatter_dose(dg_scatter* s, const double* x, uint64_t x_len, double* y, uint32_t flags,
                     void* stream) {
+  dg::DeviceGuard device_guard;  // the caller's current device is restored on return
   if (!s || (!x && s->cols) || (!y && s->rows)) return DG_ERR_INVALID_CONFIG;
   if (x_len != s->cols) return DG_ERR_DIMENSION_MISMATCH;
   DG_CUDA(cudaSetDevice(s->device));
