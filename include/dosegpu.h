@@ -63,7 +63,9 @@ enum {
   /* library-specific */
   DG_ERR_NO_DEVICE = 900,
   DG_ERR_OUT_OF_MEMORY = 901,
-  DG_ERR_CUDA_BASE = 1000 /* + cudaError_t */
+  DG_ERR_NO_NCCL = 902,      /* DG_GATHER_NCCL requested, libnccl.so.2 not loadable */
+  DG_ERR_CUDA_BASE = 1000,   /* + cudaError_t */
+  DG_ERR_NCCL_BASE = 2000    /* + ncclResult_t */
 };
 
 /* ---- the native encoding (ddm::CsrMatrix, sparse.hpp:93-108) ----------------------------- */
@@ -213,6 +215,54 @@ typedef struct {
   uint64_t rows, nnz;
 } dg_kernel_time;
 int dg_kernel_times(const dg_handle* h, dg_kernel_time* out, uint32_t cap, uint32_t* n_out);
+
+/* ---- one process, several GPUs --------------------------------------------- */
+/* The reference fans one dose out over threads behind a single call (ddm::spmv_rowchunk,
+ * include/ddm/spmv.hpp:37 -> parallel_blocks, src/spmv.cpp:17-32, 105-107).  dg_multi does the
+ * same over GPUs: the rows are cut into n_devices nnz-balanced contiguous shards
+ * (dg_partition_rows), one dg_handle per device holds its shard plus a replicated x, the doses
+ * run concurrently (one stream per device) and the d slices are gathered per `gather`:
+ *   DG_GATHER_NONE  d stays row-sharded on the devices (the optimiser's sharded-resident d);
+ *   DG_GATHER_PEER  allgatherv by peer copies (copy engines over NVLink / NVSwitch): every
+ *                   device ends with the full d; each shard's kernels write their rows straight
+ *                   into their own device's full d, which the peers then copy from;
+ *   DG_GATHER_NCCL  allgatherv as ncclGroupStart + one ncclBroadcast per shard (root = the
+ *                   shard's device, into d_full + row offset on every device) + ncclGroupEnd --
+ *                   no padding.  NCCL (libnccl.so.2) is loaded on first use; its failures are
+ *                   DG_ERR_NCCL_BASE + ncclResult_t.  Needs distinct devices.
+ * A device may appear several times in `devices` (virtual shards on one GPU; NONE / PEER). */
+enum { DG_MAX_DEVICES = 16 };
+enum { DG_GATHER_NONE = 0, DG_GATHER_PEER = 1, DG_GATHER_NCCL = 2 };
+typedef struct {
+  uint32_t struct_size;              /* sizeof(dg_multi_options) */
+  uint32_t n_devices;                /* 1 .. DG_MAX_DEVICES */
+  int32_t devices[DG_MAX_DEVICES];   /* CUDA ordinals of the shards, in row order */
+  uint32_t lane_width;               /* as dg_options */
+  uint32_t accumulation;             /* as dg_options */
+  uint32_t gather;                   /* DG_GATHER_* */
+} dg_multi_options;
+typedef struct dg_multi dg_multi;
+
+void dg_multi_default_options(dg_multi_options* o); /* 1 device (0), L = 32, exact, PEER */
+int dg_multi_create(const dg_csr_view* view, const dg_multi_options* opts, dg_multi** out);
+int dg_multi_create_generated(const dg_profile* beams, uint32_t n_beams, uint32_t index_bytes,
+                              const dg_multi_options* opts, dg_multi** out);
+/* d = A.x over every shard.  x: host (H2D on every device concurrently) or, with
+ * DG_X_ON_DEVICE, a device pointer on devices[0] (peer-copied to the others).  y: a host array
+ * of `rows` doubles receiving the full d (each device downloads its slice concurrently), or NULL
+ * with DG_Y_ON_DEVICE (d stays on the devices: dg_multi_device_d).  The gather runs in both
+ * cases.  Synchronous. */
+int dg_multi_dose(dg_multi* m, const double* x, uint64_t x_len, double* y, uint32_t flags);
+/* shard bounds (n_shards + 1 rows) and shard count */
+int dg_multi_bounds(const dg_multi* m, uint32_t* n_shards, uint64_t* bounds);
+int dg_multi_shard(const dg_multi* m, uint32_t i, dg_handle** shard);
+/* device pointers on shard i's device: its full d (rows doubles; filled by PEER / NCCL gathers)
+ * and its own slice (= full_d + bounds[i]) */
+int dg_multi_device_d(const dg_multi* m, uint32_t i, double** full_d, double** slice_d);
+/* CUDA-event times of the last dg_multi_dose, each the max over devices: x upload, the shard's
+ * dose kernels, gather (+ host download), total */
+int dg_multi_last_timing(const dg_multi* m, dg_timing* t);
+int dg_multi_destroy(dg_multi* m);
 
 /* Diagnostics (no reference counterpart): with DG_TRACE set at dg_create, the first tile wave
  * of every dose records a timeline -- per CTA {start ns, end ns, window-wait cycles, warp-cycles}

@@ -16,6 +16,7 @@
 #include <stdexcept>
 #include <string>
 #include <variant>
+#include <vector>
 
 #include "ddm/error.hpp"
 #include "ddm/sparse.hpp"
@@ -88,6 +89,49 @@ class DoseEngine {
 
  private:
   dg_handle* h_ = nullptr;
+  std::uint64_t rows_ = 0, cols_ = 0;
+};
+
+// Several GPUs behind one engine (dg_multi_*): the reference fans one call out over worker
+// threads (parallel_blocks, src/spmv.cpp:17-32); this fans it out over devices -- nnz-balanced
+// row shards, concurrent doses, the full d gathered on every device (PEER copies or NCCL) and
+// returned on the host.  Same bits as DoseEngine / ddm::spmv_rowchunk for any device list.
+class MultiDoseEngine {
+ public:
+  MultiDoseEngine(const ddm::CsrMatrix& m, const std::vector<int>& devices,
+                  std::uint32_t gather = DG_GATHER_PEER, const CudaConfig& cfg = {}) {
+    if (cfg.workers < 1) ddm::fail(ddm::Errc::InvalidConfig, "workers must be >= 1");
+    if (devices.empty() || devices.size() > DG_MAX_DEVICES)
+      ddm::fail(ddm::Errc::InvalidConfig, "1.." + std::to_string(DG_MAX_DEVICES) + " devices");
+    dg_multi_options o;
+    dg_multi_default_options(&o);
+    o.n_devices = static_cast<std::uint32_t>(devices.size());
+    for (std::size_t i = 0; i < devices.size(); ++i) o.devices[i] = devices[i];
+    o.lane_width = static_cast<std::uint32_t>(cfg.lane_width);
+    o.accumulation = cfg.fp32 ? DG_ACCUM_FP32 : DG_ACCUM_EXACT;
+    o.gather = gather;
+    const dg_csr_view v = view_of(m);
+    check(dg_multi_create(&v, &o, &m_), "dg_multi_create");
+    rows_ = m.rows;
+    cols_ = m.cols;
+  }
+  MultiDoseEngine(const MultiDoseEngine&) = delete;
+  MultiDoseEngine& operator=(const MultiDoseEngine&) = delete;
+  ~MultiDoseEngine() { dg_multi_destroy(m_); }
+
+  ddm::DenseVector dose(const ddm::DenseVector& x) {
+    if (x.size() != cols_)  // spmv.cpp:34-38
+      ddm::fail(ddm::Errc::DimensionMismatch, "input vector length " + std::to_string(x.size()) +
+                                                  " != matrix columns " + std::to_string(cols_));
+    ddm::DenseVector y(rows_, 0.0);
+    check(dg_multi_dose(m_, x.data(), x.size(), y.data(), 0), "dg_multi_dose");
+    return y;
+  }
+
+  dg_multi* handle() const { return m_; }
+
+ private:
+  dg_multi* m_ = nullptr;
   std::uint64_t rows_ = 0, cols_ = 0;
 };
 

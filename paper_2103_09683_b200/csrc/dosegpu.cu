@@ -229,7 +229,7 @@ int launch_tiles_cfg(Handle* h, const M& mat, const Acc* x, double* y, cudaStrea
     tr = {h->d_trace, h->d_trace + 4ull * h->sm_count};
   }
   const Carry<Acc> carry{static_cast<Acc*>(h->d_state)};
-  for (uint32_t w = 0; w < h->n_waves; ++w) {
+  for (uint32_t w = 0; w < h->n_launch_lists(); ++w) {
     if (!h->wave_tiles[w]) continue;
     const int grid = std::min<int>(h->sm_count, static_cast<int>(h->wave_tiles[w]));
     cudaLaunchConfig_t lc = {};

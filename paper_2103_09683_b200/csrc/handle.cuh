@@ -156,11 +156,14 @@ struct Handle {
     ++n_launch;
   }
 
+  // tile launch lists: one (all waves fused) or one per wave (n_waves <= kMaxWaves)
+  uint32_t n_launch_lists() const { return fused_waves ? 1u : (n_waves < kMaxWaves ? n_waves : kMaxWaves); }
+
   uint32_t expected_kernels() const {
     uint32_t n = accumulation == DG_ACCUM_FP32 ? 1 : 0;
     if (lane_width == 32) {
       for (int b = 0; b < kNumBins; ++b) n += bin_count[b] ? 1 : 0;
-      for (uint32_t w = 0; w < n_waves; ++w) n += wave_tiles[w] ? 1 : 0;
+      for (uint32_t w = 0; w < n_launch_lists(); ++w) n += wave_tiles[w] ? 1 : 0;
       n += n_dense_rows ? 1 : 0;
     } else {
       n += bin_count[kBinGeneral] ? 1 : 0;

@@ -18,11 +18,24 @@ const char* dg_strerror(int status) {
   if (status >= 1 && status <= 16) return kErrc[status - 1];
   if (status == DG_ERR_NO_DEVICE) return "NoDevice";
   if (status == DG_ERR_OUT_OF_MEMORY) return "OutOfMemory";
+  if (status == DG_ERR_NO_NCCL) return "NoNccl";
+  if (status >= DG_ERR_NCCL_BASE) return "NcclError";
   if (status >= DG_ERR_CUDA_BASE) return "CudaError";
   return "Unknown";
 }
 
-const char* dg_version(void) { return "dosegpu 0.1 (sm_100a)"; }
+const char* dg_version(void) { return "dosegpu 0.2 (sm_100a)"; }
+
+void dg_multi_default_options(dg_multi_options* o) {
+  if (!o) return;
+  *o = dg_multi_options{};
+  o->struct_size = sizeof(dg_multi_options);
+  o->n_devices = 1;
+  o->devices[0] = 0;
+  o->lane_width = 32;
+  o->accumulation = DG_ACCUM_EXACT;
+  o->gather = DG_GATHER_PEER;
+}
 
 // ddm::traffic(dims_of(m), layout_of(m)).total_bytes() -- perf_model.cpp:41-54 with
 // layout_of's 8-byte row pointers and 8-byte input/output vectors.

@@ -271,7 +271,7 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
         const uint64_t q = k + 1 < cnt[i] ? pos[off[i] + k + 1] : end;
         if (waves.size() <= k) waves.resize(k + 1);
         uint16_t flags = (k == 0 ? kSegFirst : 0) | (k + 1 == cnt[i] ? kSegLast : 0) |
-                         static_cast<uint16_t>(k << kSegWaveShift);
+                         static_cast<uint16_t>(std::min<uint32_t>(k, 255u) << kSegWaveShift);
         waves[k].push_back({p, static_cast<uint32_t>(q - p), r, static_cast<uint32_t>(base + k),
                             cext[off[i] + k].x, cext[off[i] + k].y,
                             static_cast<uint16_t>((p - rp[r]) & 31u), flags});
@@ -283,14 +283,16 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
 
   // 3. tiles
   const uint64_t xcap = (h->cols + align - 1) / align * align;  // padded x length on device
-  if (waves.size() > Handle::kMaxWaves) return DG_ERR_UNSUPPORTED_FEATURE;
   h->n_waves = static_cast<uint32_t>(waves.size());
   h->n_global_rows = global_x.size();
   // Several waves: one launch for all of them by default (fused: segment k + 1 of a row waits for
   // segment k's carried partials, Carry in spmv_tiles.cuh) -- one kernel tail instead of one per
-  // wave.  DG_FUSE_WAVES=0 keeps one launch per wave.
+  // wave.  DG_FUSE_WAVES=0 keeps one launch per wave (A/B only, up to kMaxWaves waves: a row may
+  // be cut into any number of segments -- a U32 row spanning a million columns is ~200 waves --
+  // and the fused launch has no limit on it).
   h->fused_waves = h->n_waves > 1;
-  if (const char* fw = std::getenv("DG_FUSE_WAVES")) h->fused_waves = h->fused_waves && std::atoi(fw);
+  if (const char* fw = std::getenv("DG_FUSE_WAVES"))
+    h->fused_waves = h->fused_waves && (std::atoi(fw) || h->n_waves > Handle::kMaxWaves);
   if (h->n_waves > 1 && !h->fused_waves) slices = false;  // one launch list only
   if (!global_x.empty()) slices = false;  // (DG_DENSE=0: global-x tiles need true columns)
   // Output row blocks: contiguous, byte-balanced row ranges.  A block's d is complete (and can be
@@ -478,10 +480,10 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     h->short_segments = nseg && snnz < 256ull * nseg;
     if (const char* ss = std::getenv("DG_SHORT_SEGMENTS")) h->short_segments = std::atoi(ss) != 0;
   }
-  for (uint32_t w = 0; w < NW; ++w) {
-    h->wave_nnz[w] = wnnz[w];
-    h->wave_rows[w] = wrows[w];
-    h->wave_tiles[w] = 0;
+  for (uint32_t w = 0; w < Handle::kMaxWaves; ++w) h->wave_nnz[w] = h->wave_rows[w] = h->wave_tiles[w] = 0;
+  for (uint32_t w = 0; w < NW; ++w) {  // (statistics; waves past the last slot are folded in it)
+    h->wave_nnz[std::min(w, Handle::kMaxWaves - 1)] += wnnz[w];
+    h->wave_rows[std::min(w, Handle::kMaxWaves - 1)] += wrows[w];
   }
   if (h->fused_waves) {
     h->fused_rows = lrows[0];

@@ -107,6 +107,16 @@ class _KernelTime(C.Structure):
                 ("rows", C.c_uint64), ("nnz", C.c_uint64)]
 
 
+MAX_DEVICES = 16
+GATHER_NONE, GATHER_PEER, GATHER_NCCL = 0, 1, 2
+
+
+class _MultiOptions(C.Structure):
+    _fields_ = [("struct_size", C.c_uint32), ("n_devices", C.c_uint32),
+                ("devices", C.c_int32 * MAX_DEVICES), ("lane_width", C.c_uint32),
+                ("accumulation", C.c_uint32), ("gather", C.c_uint32)]
+
+
 _LIB: Optional[C.CDLL] = None
 
 # name -> (restype, argtypes); the exported surface of include/dosegpu.h
@@ -141,6 +151,17 @@ _SIGS = {
     "dg_ipc_open": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]),
     "dg_ipc_close": (C.c_int, [C.c_void_p]),
     "dg_ipc_free": (C.c_int, [C.c_void_p]),
+    "dg_multi_default_options": (None, [C.POINTER(_MultiOptions)]),
+    "dg_multi_create": (C.c_int, [C.POINTER(_View), C.POINTER(_MultiOptions), C.POINTER(C.c_void_p)]),
+    "dg_multi_create_generated": (C.c_int, [C.POINTER(_Profile), C.c_uint32, C.c_uint32,
+                                            C.POINTER(_MultiOptions), C.POINTER(C.c_void_p)]),
+    "dg_multi_dose": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint32]),
+    "dg_multi_bounds": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32), C.c_void_p]),
+    "dg_multi_shard": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_void_p)]),
+    "dg_multi_device_d": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_void_p),
+                                    C.POINTER(C.c_void_p)]),
+    "dg_multi_last_timing": (C.c_int, [C.c_void_p, C.POINTER(_Timing)]),
+    "dg_multi_destroy": (C.c_int, [C.c_void_p]),
     "dg_strerror": (C.c_char_p, [C.c_int]),
     "dg_version": (C.c_char_p, []),
 }
@@ -293,7 +314,7 @@ class DoseEngine:
     def dose(self, x: np.ndarray, out: Optional[np.ndarray] = None) -> np.ndarray:
         """d = A.x with host arrays (H2D x, kernels, D2H d)."""
         x = np.ascontiguousarray(x, dtype=np.float64)
-        y = out if out is not None else np.empty(self.info["rows"], dtype=np.float64)
+        y = _out_array(out, self.info["rows"])
         _check(_lib().dg_dose(self._h, x.ctypes.data, len(x), y.ctypes.data, 0, None), "dg_dose")
         return y
 
@@ -361,7 +382,8 @@ class DoseEngine:
 
     def close(self) -> None:
         if self._h:
-            _lib().dg_destroy(self._h)
+            if getattr(self, "_owner", True):
+                _lib().dg_destroy(self._h)
             self._h = None
 
     def __del__(self):
@@ -375,6 +397,133 @@ class DoseEngine:
 
     def __exit__(self, *a):
         self.close()
+
+
+class MultiDoseEngine:
+    """One process, several GPUs behind one handle (dg_multi_*): the rows cut into nnz-balanced
+    shards, one per entry of ``devices`` (a device may repeat: virtual shards), doses run
+    concurrently and the d slices are gathered per ``gather`` (GATHER_NONE / GATHER_PEER /
+    GATHER_NCCL).  The reference's own fan-out, ddm::spmv_rowchunk -> parallel_blocks
+    (spmv.hpp:37, spmv.cpp:17-32), behind one call."""
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+        n = C.c_uint32()
+        _check(_lib().dg_multi_bounds(self._h, C.byref(n), None), "dg_multi_bounds")
+        b = np.empty(n.value + 1, dtype=np.uint64)
+        _check(_lib().dg_multi_bounds(self._h, C.byref(n), b.ctypes.data), "dg_multi_bounds")
+        self.bounds = b
+        self.rows = int(b[-1])
+        self.n_shards = n.value
+        sh = C.c_void_p()
+        _check(_lib().dg_multi_shard(self._h, 0, C.byref(sh)), "dg_multi_shard")
+        info = _Info()
+        _check(_lib().dg_get_info(sh, C.byref(info)), "dg_get_info")
+        self.cols = info.cols
+
+    @staticmethod
+    def _opts(devices, lane_width, accumulation, gather) -> _MultiOptions:
+        if not 1 <= len(devices) <= MAX_DEVICES:
+            raise Error(1 + Errc.InvalidConfig, f"1..{MAX_DEVICES} devices")
+        o = _MultiOptions()
+        _lib().dg_multi_default_options(C.byref(o))
+        o.n_devices = len(devices)
+        for i, d in enumerate(devices):
+            o.devices[i] = int(d)
+        o.lane_width, o.accumulation, o.gather = lane_width, accumulation, gather
+        return o
+
+    @classmethod
+    def from_csr(cls, m: CsrMatrix, devices: Sequence[int], *, gather: int = GATHER_PEER,
+                 lane_width: int = 32, accumulation: int = ACCUM_EXACT) -> "MultiDoseEngine":
+        rp = np.ascontiguousarray(m.row_ptr, dtype=np.uint64)
+        if m.col_indices.dtype == np.uint16:
+            col, csb = np.ascontiguousarray(m.col_indices), 2
+        else:
+            col, csb = np.ascontiguousarray(m.col_indices, dtype=np.uint32), 4
+        val = np.ascontiguousarray(m.values, dtype=_VDTYPE[m.precision])
+        view = _View(m.rows, m.cols, m.nnz, m.precision, 2 if m.index_width == U16 else 4, csb, 0,
+                     rp.ctypes.data, col.ctypes.data, val.ctypes.data)
+        o = cls._opts(devices, lane_width, accumulation, gather)
+        h = C.c_void_p()
+        _check(_lib().dg_multi_create(C.byref(view), C.byref(o), C.byref(h)), "dg_multi_create")
+        return cls(h)
+
+    @classmethod
+    def generate(cls, profiles, devices: Sequence[int], *, gather: int = GATHER_PEER,
+                 index_bytes: int = 0, lane_width: int = 32,
+                 accumulation: int = ACCUM_EXACT) -> "MultiDoseEngine":
+        arr, n = _profiles(profiles)
+        o = cls._opts(devices, lane_width, accumulation, gather)
+        h = C.c_void_p()
+        _check(_lib().dg_multi_create_generated(arr, n, index_bytes, C.byref(o), C.byref(h)),
+               "dg_multi_create_generated")
+        return cls(h)
+
+    def dose(self, x: np.ndarray, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """The full d on the host (each device downloads its slice)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = _out_array(out, self.rows)
+        _check(_lib().dg_multi_dose(self._h, x.ctypes.data, len(x), y.ctypes.data, 0),
+               "dg_multi_dose")
+        return y
+
+    def dose_host_ptrs(self, x_ptr: int, x_len: int, y_ptr: int) -> None:
+        _check(_lib().dg_multi_dose(self._h, C.c_void_p(x_ptr), x_len, C.c_void_p(y_ptr), 0),
+               "dg_multi_dose")
+
+    def dose_device(self, x_ptr: int, x_len: int) -> None:
+        """x on devices[0]; d stays on the devices (device_d)."""
+        _check(_lib().dg_multi_dose(self._h, C.c_void_p(x_ptr), x_len, None,
+                                    X_ON_DEVICE | Y_ON_DEVICE), "dg_multi_dose")
+
+    def device_d(self, i: int) -> tuple:
+        """(full d, this shard's slice) device pointers on shard i's device."""
+        f, s = C.c_void_p(), C.c_void_p()
+        _check(_lib().dg_multi_device_d(self._h, i, C.byref(f), C.byref(s)), "dg_multi_device_d")
+        return int(f.value), int(s.value)
+
+    def shard(self, i: int) -> "DoseEngine":
+        """Shard i as a (non-owning) DoseEngine view."""
+        sh = C.c_void_p()
+        _check(_lib().dg_multi_shard(self._h, i, C.byref(sh)), "dg_multi_shard")
+        e = DoseEngine(sh)
+        e._owner = False
+        return e
+
+    def last_timing(self) -> dict:
+        t = _Timing()
+        _check(_lib().dg_multi_last_timing(self._h, C.byref(t)), "dg_multi_last_timing")
+        return {"ms_h2d": t.ms_h2d, "ms_kernels": t.ms_kernels, "ms_d2h": t.ms_d2h,
+                "ms_total": t.ms_total}
+
+    def close(self) -> None:
+        if self._h:
+            _lib().dg_multi_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def _out_array(out: Optional[np.ndarray], n: int) -> np.ndarray:
+    """A caller-supplied output array must be a writable, C-contiguous float64 array of n
+    elements: the library writes n doubles through its pointer."""
+    if out is None:
+        return np.empty(n, dtype=np.float64)
+    if not isinstance(out, np.ndarray) or out.dtype != np.float64 or out.size != n \
+            or not out.flags.c_contiguous or not out.flags.writeable:
+        raise ValueError(f"out must be a writable C-contiguous float64 array of {n} elements")
+    return out
 
 
 class PeerBuffer:

@@ -95,6 +95,24 @@ int main() {
     }
     check(threw, "DimensionMismatch");
   }
+  // the multi-device engine: shards on a device list (virtual shards on one GPU: PEER / NONE
+  // gathers), same bits as the CPU engine
+  {
+    const ddm::CsrMatrix m = ddm::generate(ddm::liver_desk_profile(), ddm::ValuePrecision::Half);
+    const ddm::DenseVector x = ddm::seeded_vector(m.cols, 42);
+    const auto cpu = ddm::spmv_rowchunk(m, x, {32, 4});
+    for (std::uint32_t gather : {DG_GATHER_PEER, DG_GATHER_NONE}) {
+      ddm_cuda::MultiDoseEngine eng(m, {0, 0, 0}, gather);
+      check(bit_equal(cpu, eng.dose(x)), "multi-device engine gather " + std::to_string(gather));
+    }
+    bool threw = false;
+    try {
+      ddm_cuda::MultiDoseEngine eng(m, {0, 0}, DG_GATHER_NCCL);  // one rank per GPU
+    } catch (const ddm::Error& e) {
+      threw = e.code() == ddm::Errc::InvalidConfig;
+    }
+    check(threw, "NCCL gather with a repeated device");
+  }
   std::printf("adapter_test: %d passed, %d failed\n", g_pass, g_fail);
   return g_fail ? 1 : 0;
 }

@@ -125,3 +125,40 @@ def test_no_device_fails_loudly(port):
     assert e.value.status == 900
     with pytest.raises(dg.Error):
         dg.DoseEngine.generate(dg.profiles.liver_desk())
+    with pytest.raises(dg.Error) as e:  # the multi-device handle too
+        dg.MultiDoseEngine.from_csr(cm, [0, 0])
+    assert e.value.status == 900
+    with pytest.raises(dg.Error) as e:
+        dg.MultiDoseEngine.generate(dg.profiles.liver_desk(), [0])
+    assert e.value.status == 900
+
+
+def test_multi_options_and_status_codes():
+    o = D._MultiOptions()
+    D._lib().dg_multi_default_options(C.byref(o))
+    assert o.struct_size == C.sizeof(D._MultiOptions) == 4 * (2 + 16 + 3)
+    assert (o.n_devices, o.devices[0], o.lane_width, o.accumulation, o.gather) == \
+        (1, 0, 32, 0, dg.GATHER_PEER)
+    lib = D._lib()
+    assert lib.dg_strerror(902).decode() == "NoNccl"
+    assert lib.dg_strerror(2003).decode() == "NcclError"
+    assert lib.dg_strerror(1002).decode() == "CudaError"
+    # option errors come before any device work: a bad struct size is InvalidConfig
+    o.struct_size = 4
+    h = C.c_void_p()
+    view = D._View()
+    assert lib.dg_multi_create(C.byref(view), C.byref(o), C.byref(h)) == 1 + dg.Errc.InvalidConfig
+    o.struct_size = C.sizeof(D._MultiOptions)
+    o.n_devices = 0
+    assert lib.dg_multi_create(C.byref(view), C.byref(o), C.byref(h)) == 1 + dg.Errc.InvalidConfig
+    o.n_devices, o.gather = 1, 7
+    assert lib.dg_multi_create(C.byref(view), C.byref(o), C.byref(h)) == 1 + dg.Errc.InvalidConfig
+
+
+def test_out_array_is_checked():
+    """DoseEngine.dose(out=...) hands out's pointer to the library: a wrong dtype, size or
+    layout must raise instead of letting the library write past the buffer."""
+    D._out_array(np.empty(5), 5)
+    for bad in (np.empty(5, dtype=np.float32), np.empty(4), np.empty(10)[::2], np.empty(6)):
+        with pytest.raises(ValueError):
+            D._out_array(bad, 5)

@@ -449,6 +449,47 @@ def test_windowed_tiles_with_split_rows_bit_exact(port, monkeypatch, tile_nnz, f
     assert np.max(np.abs(gf - want)) <= FP32_TOL * np.max(np.abs(want))
 
 
+def test_u32_rows_spanning_a_million_columns_bit_exact(port, monkeypatch):
+    """No limit on the segments of a row: U32 rows scattered over ~1M columns are cut into
+    ~200 windowed segments (waves) carrying their lane partials (plan.cu returned
+    UnsupportedFeature past 64).  Reference: rowchunk_rows handles every valid CsrMatrix
+    (src/spmv.cpp:48-68)."""
+    rng = np.random.default_rng(11)
+    rows, cols = 1500, 1_000_003
+    lens = np.where(rng.random(rows) < 0.4, 0, rng.integers(1, 600, rows))
+    wide = rng.choice(rows, 25, replace=False)
+    lens[wide] = rng.integers(2000, 9000, len(wide))
+    lens[0] = 40_000  # a dense row wider than a window
+    rp = np.zeros(rows + 1, dtype=np.uint64)
+    np.cumsum(lens, out=rp[1:])
+    col = np.empty(int(rp[-1]), dtype=np.uint32)
+    for r in range(rows):
+        n = int(lens[r])
+        if n == 0:
+            continue
+        if r in wide:
+            c = np.sort(rng.choice(cols, n, replace=False))
+        elif r == 0:
+            c = np.arange(500_000, 500_000 + n)
+        else:
+            lo = int(rng.integers(0, cols - 4096))
+            c = np.sort(rng.choice(4096, n, replace=False)) + lo
+        col[rp[r]:rp[r + 1]] = c
+    vals = (rng.random(len(col)) * 0.999 + 2 ** -14).astype(np.float16).view(np.uint16)
+    m = Csr(rows, cols, HALF, U32, rp, col, vals)
+    x = port.seeded_vector(cols, 42)
+    want = port.spmv_rowchunk(m, x, 32, 4)
+    for fuse in ("1", "0"):  # DG_FUSE_WAVES=0 is overridden past 64 waves (one fused launch)
+        monkeypatch.setenv("DG_FUSE_WAVES", fuse)
+        with dg.DoseEngine.from_csr(to_dg(m)) as e:
+            assert np.array_equal(bits(e.dose(x)), bits(want))
+            x2 = port.seeded_vector(cols, 9)
+            assert np.array_equal(bits(e.dose(x2)), bits(port.spmv_rowchunk(m, x2, 32, 4)))
+    with dg.DoseEngine.from_csr(to_dg(m), accumulation=dg.ACCUM_FP32) as e:
+        gf = e.dose(x)
+    assert np.max(np.abs(gf - want)) <= FP32_TOL * np.max(np.abs(want))
+
+
 @pytest.mark.parametrize("env", [{}, {"DG_DENSE": "1"}, {"DG_DENSE": "0"},
                                  {"DG_DENSE": "1", "DG_DENSE_MIN_LEN": "1024"}])
 def test_dense_rows_kernel_bit_exact(port, monkeypatch, env):
