@@ -47,7 +47,13 @@ def parse_args():
     ap.add_argument("--no-alt-fp32", action="store_true", help="skip the fp32-family side line")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--cpu-sample-rows", type=int, default=250_000)
-    ap.add_argument("--e2e-steps", type=int, default=0, help="default: min(steps, 10)")
+    ap.add_argument("--e2e-steps", type=int, default=0, help="default: --steps")
+    ap.add_argument("--engine", default="shard", choices=["shard", "multi"],
+                    help="shard: one process per GPU (torchrun for N > 1); multi: one process "
+                         "driving --gpus devices through the dg_multi handle (DG_BENCH_DEVICES="
+                         "0,0,... lists them explicitly, e.g. virtual shards on one GPU)")
+    ap.add_argument("--gather", default="peer", choices=["none", "peer", "nccl"],
+                    help="--engine multi: the d gather of each step")
     return ap.parse_args()
 
 
@@ -148,8 +154,47 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------- CPU baselines ------
+def host_description() -> dict:
+    """The box's host side: CPU model, sockets, NUMA nodes, threads, glibc."""
+    import glob
+    import platform
+    d = {"threads": os.cpu_count()}
+    try:
+        with open("/proc/cpuinfo") as f:
+            txt = f.read()
+        models = [ln.split(":", 1)[1].strip() for ln in txt.splitlines() if ln.startswith("model name")]
+        d["cpu_model"] = models[0] if models else platform.processor()
+        phys = {ln.split(":", 1)[1].strip() for ln in txt.splitlines() if ln.startswith("physical id")}
+        d["sockets"] = len(phys) or 1
+    except Exception:
+        d["cpu_model"] = platform.processor()
+    d["numa_nodes"] = len(glob.glob("/sys/devices/system/node/node[0-9]*")) or 1
+    try:
+        d["glibc"] = os.confstr("CS_GNU_LIBC_VERSION")
+    except Exception:
+        d["glibc"] = " ".join(platform.libc_ver())
+    return d
+
+
+def cpu_oracle_single_thread(m, target_s: float = 3.0) -> dict:
+    """ddm::run_bench(Algorithm::Oracle, workers 1) on the same sample -- SURVEY 8(d) CPU row (2)."""
+    from oracle.oracle import Oracle, have_reference, traffic_bytes
+    if not have_reference():
+        return {"value": None, "error": "oracle/_ref not built"}
+    orc = Oracle("reference")
+    t1 = orc.run_bench(m, algorithm=0, lane_width=1, workers=1, reps=1, warmup=0,
+                       vector_seed=42)["mean_seconds"]
+    reps = max(1, min(20, int(target_s / max(t1, 1e-6))))
+    r = orc.run_bench(m, algorithm=0, lane_width=1, workers=1, reps=reps, warmup=1,
+                      vector_seed=42)
+    b = traffic_bytes(m.rows, m.cols, m.nnz, 2, 2 if m.cols < 65536 else 4)
+    return {"value": b / r["mean_seconds"] / 1e9, "unit": "GB/s", "cores": 1,
+            "ms_per_eval": r["mean_seconds"] * 1e3,
+            "sample": f"same sample, ddm::run_bench oracle workers=1 reps={reps} warmup=1"}
+
+
 def cpu_reference_run(ps, sample_rows: int, reps: int, warmup: int,
-                      target_s: float = 0.0) -> dict:
+                      target_s: float = 0.0, with_oracle_row: bool = False) -> dict:
     """The reference's own CPU dose path, unmodified (oracle/_ref = /root/reference/proj built
     by oracle/Makefile): ddm::generate on a row sample of the workload's profile, then
     ddm::run_bench(RowChunk, lane_width 32, workers = all host threads) -- bench.cpp:38-103.
@@ -185,8 +230,14 @@ def cpu_reference_run(ps, sample_rows: int, reps: int, warmup: int,
         del np
     vb, ib = 2, (2 if m.cols < 65536 else 4)
     b = traffic_bytes(m.rows, m.cols, m.nnz, vb, ib)
+    extra = {}
+    if with_oracle_row:
+        try:
+            extra["oracle_workers1"] = cpu_oracle_single_thread(m)
+        except Exception as ex:  # reported, never silently replaced
+            extra["oracle_workers1"] = {"value": None, "error": str(ex)[:200]}
     return {"value": b / mean_s / 1e9, "unit": "GB/s", "cores": cores, "kind": kind,
-            "ms_per_eval": mean_s * 1e3, "model_bytes": b,
+            "ms_per_eval": mean_s * 1e3, "model_bytes": b, "host": host_description(), **extra,
             "sample": f"ddm::generate rows={sample_rows} of the workload profile "
                       f"({m.nnz} nnz, {b / 1e9:.3f} GB model bytes), ddm::run_bench rowchunk "
                       f"L=32 workers={cores}, reps={reps} warmup={warmup}"}
@@ -227,7 +278,7 @@ def run_reference(args):
             "ms_per_step": r["ms_per_eval"], "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator)",
             "config": {"workload": workload_desc(args.config, ps), "sample_rows": args.cpu_sample_rows},
-            "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample", "host")},
             "e2e": {"value": r["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -346,7 +397,7 @@ def run_ours(args):
     dom_name, dom = max(per.items(), key=lambda kv: kv[1]["ms"])
 
     # end to end through the public API: pinned host x and d, H2D + kernels + D2H timed
-    e2e_steps = args.e2e_steps or min(args.steps, 10)
+    e2e_steps = args.e2e_steps or args.steps
     xh = torch.from_numpy(x_host).pin_memory()
     yhs = [torch.empty(e.info["rows"], dtype=torch.float64).pin_memory() for e in engines]
 
@@ -497,8 +548,10 @@ def run_ours(args):
         engines = fengs
     if world == 1 and not args.no_cpu_baseline:
         try:
-            r = cpu_reference_run(ps, args.cpu_sample_rows, 5, 1, target_s=10.0)
-            line["cpu_baseline"] = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            r = cpu_reference_run(ps, args.cpu_sample_rows, 5, 1, target_s=10.0,
+                                  with_oracle_row=True)
+            line["cpu_baseline"] = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample",
+                                                      "host", "oracle_workers1") if k in r}
         except Exception as ex:  # reported, never silently replaced
             line["cpu_baseline"] = {"value": None, "error": str(ex)[:200]}
     else:
@@ -510,10 +563,102 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_multi(args):
+    """--engine multi: one process drives every device through the dg_multi handle (the C-ABI
+    multi-GPU product path).  A step = dg_multi_dose with x on devices[0]: x peer-copied to every
+    device, the shards' doses run concurrently, then the --gather exchange; timed per step with
+    CUDA events on every device (max over devices, dg_multi_last_timing)."""
+    import numpy as np
+    import torch
+
+    import paper_2103_09683_b200 as dg
+
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        raise SystemExit("--engine multi is one process (no torchrun)")
+    devs = os.environ.get("DG_BENCH_DEVICES")
+    devices = [int(d) for d in devs.split(",")] if devs else list(range(args.gpus))
+    gather = {"none": dg.GATHER_NONE, "peer": dg.GATHER_PEER, "nccl": dg.GATHER_NCCL}[args.gather]
+    accum = dg.ACCUM_EXACT if args.accum == "exact" else dg.ACCUM_FP32
+    ps = workload(args.config, args.rows)
+    if args.config == "c5":
+        raise SystemExit("--engine multi: c1 / c2 / c4")
+    cols = sum(p.cols for p in ps)
+    torch.cuda.set_device(devices[0])
+    t0 = time.time()
+    m = dg.MultiDoseEngine.generate(ps, devices, gather=gather, accumulation=accum)
+    setup_s = time.time() - t0
+    shards = [m.shard(i) for i in range(m.n_shards)]
+    model_bytes = sum(e.info["model_bytes"] for e in shards)
+    x_host = dg.seeded_vector(cols, 42)
+    x = torch.from_numpy(x_host).cuda()
+
+    def run(n, fn):
+        tot = ker = 0.0
+        for _ in range(n):
+            fn()
+            t = m.last_timing()
+            tot += t["ms_total"]
+            ker += t["ms_kernels"]
+        return tot, ker
+
+    for _ in range(max(args.warmup, 3)):
+        m.dose_device(x.data_ptr(), cols)
+    clocks = ClockSampler(devices[0])
+    clocks.wait_ready()
+    clocks.mark_start()
+    ms, kms = run(args.steps, lambda: m.dose_device(x.data_ptr(), cols))
+    clocks.mark_stop()
+    clk = clocks.stop()
+    xh = torch.from_numpy(x_host).pin_memory()
+    yh = torch.empty(m.rows, dtype=torch.float64).pin_memory()
+    m.dose_host_ptrs(xh.data_ptr(), cols, yh.data_ptr())
+    e2e_ms, _ = run(args.steps, lambda: m.dose_host_ptrs(xh.data_ptr(), cols, yh.data_ptr()))
+    full, _ = m.device_d(0)
+    if gather != dg.GATHER_NONE:
+        d0 = torch.empty(m.rows, dtype=torch.float64, device=f"cuda:{devices[0]}")
+        torch.cuda.synchronize()
+        d0.copy_(torch.as_tensor(_DevView(full, m.rows), device=f"cuda:{devices[0]}"))
+        assert np.array_equal(d0.cpu().numpy().view(np.uint64), yh.numpy().view(np.uint64)), \
+            "gathered d on device 0 differs from the host d"
+    ms_step, e2e_step_ms = ms / args.steps, e2e_ms / args.steps
+    n_phys = len(set(devices))
+    line = {
+        "metric": metric_name(args.config), "engine": "multi (dg_multi, one process)",
+        "value": model_bytes / (ms_step * 1e-3) / 1e9, "unit": "GB/s", "n_gpus": n_phys,
+        "shards": len(devices), "devices": devices, "gather": args.gather,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_step,
+        "ms_per_step_kernels": kms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64" if accum == dg.ACCUM_EXACT else "f32",
+        "data": "synthetic (row-parallel device generator, reference profile statistics)",
+        "config": {"workload": workload_desc(args.config, ps), "rows": m.rows, "cols": cols,
+                   "parallelism": f"row-shard x{len(devices)} over {n_phys} device(s), "
+                                  f"gather {args.gather}",
+                   "model_bytes_per_step": int(model_bytes), "l2": "inputs larger than L2",
+                   "setup_s": round(setup_s, 2)},
+        "e2e": {"value": model_bytes / (e2e_step_ms * 1e-3) / 1e9, "unit": "GB/s",
+                "ms_per_step": e2e_step_ms, "h2d_bytes_per_step": 8 * cols * len(devices),
+                "d2h_bytes_per_step": 8 * m.rows},
+        "gpu_launches": sum(int(e.info["n_kernels"]) for e in shards) * args.steps,
+        "clocks": clk, "cpu_baseline": None,
+    }
+    print(json.dumps(line), flush=True)
+    m.close()
+
+
+class _DevView:
+    """A raw device pointer as a __cuda_array_interface__ (float64[n])."""
+
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False),
+                                         "version": 2, "strides": None}
+
+
 def main():
     args = parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.engine == "multi":
+        run_multi(args)
     else:
         run_ours(args)
 

@@ -59,10 +59,12 @@ struct Handle {
   static constexpr int kSliceWarpsCarry = 20;  // ... with carried partials (split rows)
   bool slices_wanted = false;      // plan for the slice stream (DG_SLICES=0: row-ordered k_tiles)
   bool slices = false;             // the plan has one; d_slices holds it
+  static constexpr int kRunsPerWarp = 2;     // runs per tile = kRunsPerWarp x warps (pulled dynamically)
   int slice_warps = 0;
+  int slice_runs = 0;
   uint64_t slice_chunks = 0;       // 32-word chunks in the stream
   uint32_t* d_slices = nullptr;
-  void* d_ranges = nullptr;        // WarpRange[tiles * warps + 1]
+  void* d_ranges = nullptr;        // WarpRange[tiles * runs + 1]
   void* d_sseg = nullptr;          // SliceSeg per segment
   uint64_t n_segments = 0;         // segments of launch list 0
   // with slices the handle's stream (d_packed / d_col / d_val, d_row_ptr) is the REST stream of

@@ -250,6 +250,10 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     if (st == DG_OK) {
       cu(cudaMemcpy(d_rows, wide.data(), wide.size() * 4, cudaMemcpyHostToDevice));
       cu(cudaMemcpy(d_off, off.data(), (wide.size() + 1) * 8, cudaMemcpyHostToDevice));
+      // (rows fill only their first count[i] slots; the rest is copied back unread -- zeroed so
+      //  the copy reads initialised memory, compute-sanitizer initcheck)
+      cu(cudaMemset(d_pos, 0, total * 8));
+      cu(cudaMemset(d_cext, 0, total * sizeof(uint2)));
       k_split_rows<M><<<grid_for(wide.size(), 128), 128>>>(
           mat, h->d_row_ptr, d_rows, static_cast<uint32_t>(wide.size()),
           d_off, A, d_pos, d_cext, d_cnt);
@@ -410,7 +414,10 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     auto cls = [&](const HostSeg& q) -> int {
       const uint32_t span = q.chi - q.clo + 1;
       // (slot mode on the row-ordered stream: Packed16 only -- k_assign_slots rewrites it)
-      if (rep && (slices || h->packed) && span <= A3 && 4ull * q.n < 3ull * span) return 0;
+      // (dense segments too: a row 75-99% dense spreads a half-warp's 16 lanes over ~16-21
+      //  columns, so without replicas two of them often share a bank pair; fully dense rows
+      //  gain nothing but lose nothing either)
+      if (rep && (slices || h->packed) && span <= A3) return 0;
       return narrow(q) ? 1 : 2;
     };
     auto bin = [&](const HostSeg& q, int c) -> uint32_t {

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
 #include <vector>
 
@@ -13,20 +14,25 @@
 
 namespace dg {
 
-// ---- plan: segments of every tile assigned to the CTA's warps --------------------------------
-// LPT on chunks (longest segment to the least-loaded warp): a warp's run ends when its last
-// segment does, and the tile's window is released when the slowest warp is done.  The tile's
-// segment list is reordered warp by warp; each run is padded to whole batches.
+// ---- plan: segments of every tile grouped into runs ------------------------------------------
+// A tile's segments are grouped into R = kRunsPerWarp x WARPS runs by LPT on chunks (longest
+// segment to the least-loaded run), the runs listed longest first; the CTA's warps pull runs
+// dynamically, so the runs still left when a warp frees up are the shortest (online LPT): the
+// tile's window is released when the slowest warp is done, and a static run per warp left ~25% of
+// warp time waiting on a window on C2's 1/8 shard (DG_TRACE).  Each run is padded to whole
+// 4-chunk blocks (512 B).
 int plan_slices(Handle* h, const std::vector<Tile>& tiles, std::vector<Segment>& segs) {
   const int WARPS = h->n_carry_slots ? Handle::kSliceWarpsCarry : Handle::kSliceWarps;
+  int RUNS = WARPS * Handle::kRunsPerWarp;
+  if (const char* rw = std::getenv("DG_RUNS_PER_WARP")) RUNS = WARPS * std::max(1, std::atoi(rw));
   std::vector<WarpRange> R;
-  R.reserve(tiles.size() * WARPS + 1);
+  R.reserve(tiles.size() * RUNS + 1);
   std::vector<SliceSeg> ss(segs.size());
   std::vector<Segment> out(segs.size());
   uint64_t chunk = 0;
-  std::vector<uint32_t> idx;
-  std::vector<std::vector<uint32_t>> lists(WARPS);
-  std::vector<uint64_t> load(WARPS);
+  std::vector<uint32_t> idx, order(RUNS);
+  std::vector<std::vector<uint32_t>> lists(RUNS);
+  std::vector<uint64_t> load(RUNS);
   auto nch = [](const Segment& s) { return (static_cast<uint32_t>(s.lane0) + s.n + 31) / 32; };
   for (const Tile& T : tiles) {
     idx.resize(T.seg1 - T.seg0);
@@ -40,8 +46,11 @@ int plan_slices(Handle* h, const std::vector<Tile>& tiles, std::vector<Segment>&
       lists[w].push_back(i);
       load[w] += nch(segs[i]);
     }
+    std::iota(order.begin(), order.end(), 0u);
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return load[a] > load[b]; });
     uint32_t k = T.seg0;
-    for (int w = 0; w < WARPS; ++w) {
+    for (int q = 0; q < RUNS; ++q) {
+      const uint32_t w = order[q];
       R.push_back({static_cast<uint32_t>(chunk), k});
       for (uint32_t i : lists[w]) {
         const Segment& S = segs[i];
@@ -49,13 +58,14 @@ int plan_slices(Handle* h, const std::vector<Tile>& tiles, std::vector<Segment>&
         ss[k] = {S.row, S.slot, nch(S), S.flags};
         ++k;
       }
-      chunk += (load[w] + kSliceU - 1) / kSliceU * kSliceU;
+      chunk += (load[w] + kSlicePad - 1) / kSlicePad * kSlicePad;
       if (chunk > 0xFFFFFFFFull) return DG_ERR_UNSUPPORTED_FEATURE;
     }
   }
   R.push_back({static_cast<uint32_t>(chunk), static_cast<uint32_t>(segs.size())});
   segs.swap(out);
   h->slice_warps = WARPS;
+  h->slice_runs = RUNS;
   h->slice_chunks = chunk;
   DG_CUDA(cudaMalloc(&h->d_ranges, R.size() * sizeof(WarpRange)));
   DG_CUDA(cudaMemcpy(h->d_ranges, R.data(), R.size() * sizeof(WarpRange), cudaMemcpyHostToDevice));
@@ -68,7 +78,7 @@ int plan_slices(Handle* h, const std::vector<Tile>& tiles, std::vector<Segment>&
 
 namespace {
 
-// One warp per (tile, warp) run: the run's chunks in the lane-major block layout.  Slot-mode
+// One warp per (tile, run) run: the run's chunks in the lane-major block layout.  Slot-mode
 // tiles (nrep > 1) choose every position's replica with the per-half-warp b-matching
 // (HalfMatch), solved by the half's first lane.
 template <class M>
@@ -221,7 +231,7 @@ int build_slices(Handle* h) {
   const uint64_t words = h->slice_chunks * 32;
   DG_CUDA(cudaMalloc(&h->d_slices, std::max<uint64_t>(words, 4) * 4));
   const uint32_t zero_slot = h->window_cols - 1;
-  const uint32_t n_runs = h->wave_tiles[0] * h->slice_warps;
+  const uint32_t n_runs = h->wave_tiles[0] * h->slice_runs;
   // rest rows: non-empty rows no segment belongs to
   std::vector<uint64_t> rp(h->rows + 1);
   DG_CUDA(cudaMemcpy(rp.data(), h->d_row_ptr, (h->rows + 1) * 8, cudaMemcpyDeviceToHost));
@@ -256,7 +266,7 @@ int build_slices(Handle* h) {
         if (n_runs)
           k_build_slices<M><<<grid_for(32ull * n_runs, 256, 8), 256>>>(
               mat, static_cast<const Tile*>(h->d_tiles[0]), static_cast<const Segment*>(h->d_segs[0]),
-              static_cast<const WarpRange*>(h->d_ranges), n_runs, h->slice_warps, h->d_slices,
+              static_cast<const WarpRange*>(h->d_ranges), n_runs, h->slice_runs, h->d_slices,
               h->rep_stride, zero_slot);
         if (rest_nnz)
           k_copy_rest<M><<<grid_for(32ull * h->rows, 256, 8), 256>>>(mat, h->d_row_ptr, d_rest_rp,
@@ -296,11 +306,11 @@ int decode_rows(const Handle* h, uint64_t r0, uint64_t r1, uint32_t* d_col, uint
   DG_CUDA(cudaMemcpy(&b, h->d_row_ptr_orig + r0, 8, cudaMemcpyDeviceToHost));
   DG_CUDA(cudaMemcpy(&e, h->d_row_ptr_orig + r1, 8, cudaMemcpyDeviceToHost));
   if (e == b) return DG_OK;
-  const uint32_t n_runs = h->wave_tiles[0] * h->slice_warps;
+  const uint32_t n_runs = h->wave_tiles[0] * h->slice_runs;
   if (n_runs)
     k_decode_slices<<<grid_for(32ull * n_runs, 256, 8), 256>>>(
         h->d_slices, static_cast<const Tile*>(h->d_tiles[0]), static_cast<const Segment*>(h->d_segs[0]),
-        static_cast<const WarpRange*>(h->d_ranges), n_runs, h->slice_warps, h->rep_stride, b, e,
+        static_cast<const WarpRange*>(h->d_ranges), n_runs, h->slice_runs, h->rep_stride, b, e,
         d_col, d_val);
   if (h->rest_nnz) {
     const int st = dispatch_mat(h, [&](const auto& mat) {
@@ -364,6 +374,7 @@ int launch_slices(Handle* h, const Acc* x, double* y, cudaStream_t s) {
   }
   DG_CUDA(cudaLaunchKernelEx(&lc, kern, reinterpret_cast<const uint4*>(h->d_slices), xsrc,
                              static_cast<const Tile*>(h->d_tiles[0]), h->wave_tiles[0],
+                             static_cast<uint32_t>(h->slice_runs),
                              static_cast<const WarpRange*>(h->d_ranges),
                              static_cast<const SliceSeg*>(h->d_sseg), cr, y, h->d_counters,
                              h->window_cols, sig, h->gt, tr));

@@ -1,8 +1,9 @@
 // spmv_slices.cuh -- the tile kernel over the slice stream (warp-contiguous, 128-bit streaming).
 //
 // The slice stream is the binary16 matrix re-laid out once at dg_create for the tile kernel:
-//   * per tile, per warp of the CTA, one contiguous run of 8-chunk batches (the plan assigns the
-//     tile's segments to warps, LPT on chunks), tiles in claim order;
+//   * per tile, 2 x warps contiguous runs of 4-chunk blocks (the plan groups the tile's segments
+//     into runs, LPT on chunks, longest run first; the CTA's warps pull runs dynamically), tiles in
+//     claim order;
 //   * a chunk is 32 words, one per logical lane of ONE segment: word l of a segment's chunk j is
 //     the nonzero at position base0 + 32 j + l (base0 = the row's lane grid, Segment::lane0), so
 //     lane l still owns the reference's lane l (positions start + l, start + l + 32, ...);
@@ -15,8 +16,8 @@
 //     8 chunks is two fully coalesced LDG.128 per lane, aligned to 128-byte lines.
 // Compared with the row-ordered stream (k_tiles): no segment-edge lines fetched twice (adjacent
 // rows of the row-ordered stream sit in unrelated tiles), no misaligned 2-line chunk requests, no
-// masked edge batches; the price is the neutral padding (< 32 words per segment end, < 8 chunks
-// per warp range).  Results are bit-identical: each lane adds the same products in the same
+// masked edge batches; the price is the neutral padding (< 32 words per segment end, < 4 chunks
+// per run).  Results are bit-identical: each lane adds the same products in the same
 // order from +0.0, and a neutral word adds +0 * (+0.0) = +0.0, the identity of an accumulator
 // that is never -0.0.
 #pragma once
@@ -41,7 +42,12 @@ struct SliceSeg {
   uint32_t flags;  // kSegFirst | kSegLast
 };
 
-constexpr int kSliceU = 8;  // chunks per batch (two 512-byte blocks)
+constexpr int kSliceU = 8;      // chunks per batch (two 512-byte blocks)
+#ifndef DG_SLICE_PAD
+#define DG_SLICE_PAD 4
+#endif
+constexpr int kSliceBlock = 4;  // chunks per block
+constexpr int kSlicePad = DG_SLICE_PAD;  // runs are padded to whole multiples of this many chunks
 
 __device__ __forceinline__ uint4 ld_stream16(const uint4* p) {
   uint4 v;
@@ -51,17 +57,20 @@ __device__ __forceinline__ uint4 ld_stream16(const uint4* p) {
   return v;
 }
 
-// One warp's run: nb batches starting at chunk c0.  Software pipeline: batch b + 1 is in flight
-// in registers while batch b is gathered and accumulated; lanes 0..7 prefetch the 8 lines of
-// batch b + 1 + P into L2.
+// One warp's run: nblk 4-chunk blocks starting at chunk c0 (a multiple of 4), consumed in batches
+// of two blocks; an odd last block is paired with neutral words (`neutral`: the zero slot, value
+// +0).  Software pipeline: batch b + 1 is in flight in registers while batch b is gathered and
+// accumulated; lanes 0..7 prefetch the 8 lines of batch b + 1 + P into L2.
 template <typename Acc, int P, bool CARRY>
-__device__ __forceinline__ void run_slice(const uint4* __restrict__ blocks, uint32_t c0, uint32_t nb,
+__device__ __forceinline__ void run_slice(const uint4* __restrict__ blocks, uint32_t c0, uint32_t nblk,
                                           const SliceSeg* __restrict__ sseg, uint32_t s0,
-                                          uint32_t s1, const Acc* xs, const Carry<Acc>& carry,
-                                          double* __restrict__ y, const GatherTargets& gt,
-                                          uint32_t lane) {
+                                          uint32_t s1, const Acc* xs, uint32_t neutral,
+                                          const Carry<Acc>& carry, double* __restrict__ y,
+                                          const GatherTargets& gt, uint32_t lane) {
   using Ops = AccOps<Acc>;
-  if (nb == 0) return;
+  if (nblk == 0) return;
+  const uint32_t nb = (nblk + 1) / 2;  // batches
+  const uint4 pad = make_uint4(neutral, neutral, neutral, neutral);
   // current segment and the next one's descriptor (loaded one segment ahead)
   uint32_t si = s0;
   SliceSeg cur = sseg[si];
@@ -69,11 +78,13 @@ __device__ __forceinline__ void run_slice(const uint4* __restrict__ blocks, uint
   uint32_t left = cur.nch;
   Acc acc = CARRY ? carry.in(cur.slot, cur.flags, lane) : Acc(0);
   const uint4* p = blocks + static_cast<uint64_t>(c0 / 4) * 32 + lane;  // block c0/4, lane's 16 B
-  uint4 a0 = ld_stream16(p), a1 = ld_stream16(p + 32), b0, b1;
+  uint4 a0 = ld_stream16(p), a1 = nblk > 1 ? ld_stream16(p + 32) : pad, b0, b1;
+  // line l (< 8) of batch k: block 2k + (l >= 4)
+  auto pf_ok = [&](uint32_t k) { return 2 * k + (lane >= 4 ? 1u : 0u) < nblk; };
   if constexpr (P > 0) {
 #pragma unroll
     for (int k = 1; k <= P; ++k)
-      if (lane < 8 && static_cast<uint32_t>(k) < nb)
+      if (lane < 8 && pf_ok(k))
         asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(p - lane + 64 * k) + 128 * lane));
   }
   auto finish = [&]() {  // the current segment ends with the chunk just added
@@ -110,6 +121,26 @@ __device__ __forceinline__ void run_slice(const uint4* __restrict__ blocks, uint
       left -= kSliceU;
       return;
     }
+#ifndef DG_SLICE_ONE_FINISH
+#define DG_SLICE_ONE_FINISH 1
+#endif
+    if (DG_SLICE_ONE_FINISH) {
+      // segment ends inside the batch: words [k, e) of the current segment are added in position
+      // order (predicated), then one finish() -- a single inlined copy of the row epilogue
+      // instead of one per word (code size: the kernel's hot loop stays in the instruction cache)
+      uint32_t k = 0;
+      do {
+        const uint32_t e = left >= kSliceU - k ? static_cast<uint32_t>(kSliceU) : k + left;
+#pragma unroll
+        for (int j = 0; j < kSliceU; ++j)
+          if (j >= static_cast<int>(k) && j < static_cast<int>(e))
+            acc = Ops::add(acc, Ops::prod(static_cast<uint16_t>(r[j] & 0xFFFFu), xv[j]));
+        left -= e - k;
+        k = e;
+        if (left == 0) finish();
+      } while (k < static_cast<uint32_t>(kSliceU));
+      return;
+    }
 #pragma unroll
     for (int k = 0; k < kSliceU; ++k) {
       acc = Ops::add(acc, Ops::prod(static_cast<uint16_t>(r[k] & 0xFFFFu), xv[k]));
@@ -121,10 +152,10 @@ __device__ __forceinline__ void run_slice(const uint4* __restrict__ blocks, uint
     // step A: consume a, load b
     if (bi + 1 < nb) {
       b0 = ld_stream16(p + 64);
-      b1 = ld_stream16(p + 96);
+      b1 = 2 * bi + 3 < nblk ? ld_stream16(p + 96) : pad;
     }
     if constexpr (P > 0)
-      if (lane < 8 && bi + 1 + P < nb)
+      if (lane < 8 && pf_ok(bi + 1 + P))
         asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(p - lane + 64 * (1 + P)) + 128 * lane));
     consume(a0, a1);
     if (++bi == nb) break;
@@ -132,10 +163,10 @@ __device__ __forceinline__ void run_slice(const uint4* __restrict__ blocks, uint
     // step B: consume b, load a
     if (bi + 1 < nb) {
       a0 = ld_stream16(p + 64);
-      a1 = ld_stream16(p + 96);
+      a1 = 2 * bi + 3 < nblk ? ld_stream16(p + 96) : pad;
     }
     if constexpr (P > 0)
-      if (lane < 8 && bi + 1 + P < nb)
+      if (lane < 8 && pf_ok(bi + 1 + P))
         asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(p - lane + 64 * (1 + P)) + 128 * lane));
     consume(b0, b1);
     if (++bi == nb) break;
@@ -148,21 +179,25 @@ __device__ __forceinline__ void run_slice(const uint4* __restrict__ blocks, uint
 template <typename Acc, int WARPS, int P, bool CARRY, int NB = 2>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     k_slices(const uint4* __restrict__ blocks, XSource<Acc> xsrc, const Tile* __restrict__ tiles,
-             uint32_t n_tiles, const WarpRange* __restrict__ ranges,
+             uint32_t n_tiles, uint32_t runs, const WarpRange* __restrict__ ranges,
              const SliceSeg* __restrict__ sseg, Carry<Acc> carry, double* __restrict__ y,
              uint32_t* __restrict__ counter, uint32_t wcap, BlockSignal sig,
              const __grid_constant__ GatherTargets gt, TileTrace tr) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t full[NB];
-  __shared__ uint32_t tile_of[NB], done[NB];
+  // full[b]: the window of buffer b has landed (TMA complete_tx); empty[b]: every warp has left
+  // buffer b (WARPS arrivals) -- the refill of b waits on it, so the window's readers are ordered
+  // before its next TMA overwrite by barrier operations (visible to compute-sanitizer racecheck)
+  __shared__ __align__(8) uint64_t full[NB], empty[NB];
+  __shared__ uint32_t tile_of[NB], done[NB], run_next[NB];
   Acc* const xbuf0 = reinterpret_cast<Acc*>(smem_raw);
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t lane = threadIdx.x & 31;
   const Acc* __restrict__ x = xsrc.x;
 
   auto refill = [&](int b) {
     const uint32_t t = atomicAdd(counter, 1u);
     tile_of[b] = t;
     done[b] = 0;
+    run_next[b] = 0;
     if (t < n_tiles) {
       const Tile T = tiles[t];
       if (tr.cta) {
@@ -186,10 +221,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
         for (uint32_t off = 0; off < bytes; off += 32768u)
           tma_load_1d(dst + off, src + off, min(32768u, bytes - off), &full[b]);
       }
-      // the first 2 KB of every warp's run and the tile's segment descriptors into L2: the
-      // warps start the tile on L2 hits
-      const WarpRange* R = ranges + static_cast<uint64_t>(t) * WARPS;
-      for (int w = 0; w < WARPS; ++w) {
+      // the first 2 KB of every run and the tile's segment descriptors into L2: the warps
+      // start the tile's runs on L2 hits
+      const WarpRange* R = ranges + static_cast<uint64_t>(t) * runs;
+      for (uint32_t w = 0; w < runs; ++w) {
         const uint32_t c = R[w].chunk, ce = R[w + 1].chunk;
         if (ce > c)
           asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(blocks + static_cast<uint64_t>(c / 4) * 32),
@@ -197,7 +232,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
                        : "memory");
       }
       const uint64_t sb = reinterpret_cast<uint64_t>(sseg + R[0].seg) & ~15ull;
-      const uint64_t se = reinterpret_cast<uint64_t>(sseg + R[WARPS].seg);
+      const uint64_t se = reinterpret_cast<uint64_t>(sseg + R[runs].seg);
       if (se > sb)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sb),
                      "r"(static_cast<uint32_t>(se - sb))
@@ -209,7 +244,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 
   if (threadIdx.x < NB) xbuf0[threadIdx.x * wcap + wcap - 1] = Acc(0);  // zero slots
   if (threadIdx.x == 0)
-    for (int i = 0; i < NB; ++i) mbar_init(&full[i], 1);
+    for (int i = 0; i < NB; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], WARPS);
+    }
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
   if (threadIdx.x == 0)
@@ -232,15 +270,30 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     phases ^= 1u << b;
     const uint32_t t = *reinterpret_cast<volatile uint32_t*>(&tile_of[b]);
     if (t >= n_tiles) break;
-    const WarpRange r0 = ranges[static_cast<uint64_t>(t) * WARPS + warp];
-    const WarpRange r1 = ranges[static_cast<uint64_t>(t) * WARPS + warp + 1];
-    run_slice<Acc, P, CARRY>(blocks, r0.chunk, (r1.chunk - r0.chunk) / kSliceU, sseg, r0.seg, r1.seg,
-                             xbuf0 + b * wcap, carry, y, gt, lane);
+    // pull the tile's runs (longest first) until none is left
+#ifndef DG_SLICE_DYN
+#define DG_SLICE_DYN 1
+#endif
+    for (uint32_t it = 0;; ++it) {
+      uint32_t k = 0;
+      if (DG_SLICE_DYN) {
+        if (lane == 0) k = atomicAdd(&run_next[b], 1u);
+        k = __shfl_sync(kFull, k, 0);
+      } else {
+        k = it == 0 ? threadIdx.x / 32 : runs;  // static: run = warp (runs == WARPS)
+      }
+      if (k >= runs) break;
+      const WarpRange r0 = ranges[static_cast<uint64_t>(t) * runs + k];
+      const WarpRange r1 = ranges[static_cast<uint64_t>(t) * runs + k + 1];
+      run_slice<Acc, P, CARRY>(blocks, r0.chunk, (r1.chunk - r0.chunk) / kSliceBlock, sseg, r0.seg,
+                               r1.seg, xbuf0 + b * wcap, (wcap - 1) << 16, carry, y, gt, lane);
+    }
     __syncwarp();
     if (lane == 0) {
       if (sig.left) __threadfence(); else __threadfence_block();
-      if (atomicAdd(&done[b], 1u) == WARPS - 1) {
-        __threadfence_block();
+      mbar_arrive(&empty[b]);  // release: this warp's reads of buffer b are done
+      if (atomicAdd(&done[b], 1u) == WARPS - 1) {  // the last warp to leave refills b
+        mbar_wait(&empty[b], ((phases >> b) & 1u) ^ 1u);  // acquire every warp's release
         const Tile T = tiles[t];
         if (tr.cta) tr.tile[3ull * t + 1] = gtimer_ns();
         if (sig.left && T.blk != kNoBlock) {

@@ -588,7 +588,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
             uint32_t* __restrict__ counter, uint32_t wcap, BlockSignal sig, const __grid_constant__ GatherTargets gt,
             TileTrace tr) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t full[NB];
+  // full[b]: the window of buffer b has landed (TMA complete_tx); empty[b]: every warp has left
+  // buffer b (WARPS arrivals) -- the refill of b waits on it, so the window's readers are ordered
+  // before its next TMA overwrite by barrier operations (visible to compute-sanitizer racecheck)
+  __shared__ __align__(8) uint64_t full[NB], empty[NB];
   __shared__ uint32_t tile_of[NB], seg_next[NB], done[NB];
   Acc* const xbuf0 = reinterpret_cast<Acc*>(smem_raw);
   const uint32_t lane = threadIdx.x & 31;
@@ -650,7 +653,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   };
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < NB; ++i) mbar_init(&full[i], 1);
+    for (int i = 0; i < NB; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], WARPS);
+    }
   }
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
@@ -694,8 +700,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     if (lane == 0) {
       // this warp's reads of buffer b (and, when signalling, its d stores) happen before the count
       if (sig.left) __threadfence(); else __threadfence_block();
+      mbar_arrive(&empty[b]);  // release: this warp's reads of buffer b are done
       if (atomicAdd(&done[b], 1u) == WARPS - 1) {  // the tile is finished
-        __threadfence_block();
+        mbar_wait(&empty[b], ((phases >> b) & 1u) ^ 1u);  // acquire every warp's release
         if (tr.cta) tr.tile[3ull * t + 1] = gtimer_ns();
         if (sig.left && T.blk != kNoBlock) {
           __threadfence();

@@ -29,6 +29,17 @@ def shard_bounds_from_row_ptr(row_ptr: np.ndarray, world: int, bytes_per_nnz: in
     return partition_rows(row_ptr, world, bytes_per_nnz)
 
 
+CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy: the legacy default stream as an explicit handle
+
+
+def _torch_stream(device: int) -> int:
+    """torch's current stream on `device` as a handle for dg_dose.  Torch's default stream is the
+    legacy stream, whose handle is 0 -- which dg_dose reads as "the handle's own stream" -- so it
+    is passed as cudaStreamLegacy instead."""
+    import torch
+    return torch.cuda.current_stream(device).cuda_stream or CUDA_STREAM_LEGACY
+
+
 def gather_dose(y_local, bounds: Sequence[int], group=None):
     """All-gather unequal d slices into the full d on every rank (torch tensors, same device as
     y_local).  Pads to the largest slice, gathers, compacts."""
@@ -76,6 +87,11 @@ class ShardedDose:
         return cls(ps, rank=rank, world=world, device=device, bounds=bounds, **kw)
 
     def _engine_local(self, x, y, stream: int = 0):
+        # default: torch's current stream on this device, so the dose is ordered after the torch
+        # work that produced x and before the torch work (all-gather, copies) that reads y
+        # (the handle's private stream would be ordered with neither -- ADVICE r01)
+        if not stream:
+            stream = _torch_stream(self.device)
         self.engine.dose_device(x.data_ptr(), x.numel(), y.data_ptr(), stream=stream, sync=False)
 
     @property
@@ -174,16 +190,24 @@ class FusedGather:
 
     def dose(self, x, y_local, *, stream: int = 0):
         """This rank's slice into y_local and into every rank's full d; returns this rank's full
-        d once every rank has finished (stream sync + barrier)."""
+        d once every rank has finished (stream sync + barrier).  The returned tensor is valid
+        until the next ``dose`` call: that call first waits at a barrier for every rank (so no
+        rank is still reading its full d from the previous dose when the peers' kernels start
+        overwriting it), then overwrites it."""
         import torch
         import torch.distributed as dist
 
+        own = not stream
+        if own:
+            stream = _torch_stream(self.device)
+        # write-after-read: every rank is done with the previous full d before anyone writes it
+        dist.barrier(group=self.group)
         self.engine.dose_device(x.data_ptr(), x.numel(), y_local.data_ptr(), stream=stream,
                                 sync=False)
-        if stream:
-            torch.cuda.ExternalStream(stream).synchronize()
+        if own:
+            torch.cuda.current_stream(self.device).synchronize()
         else:
-            torch.cuda.synchronize()
+            torch.cuda.ExternalStream(stream).synchronize()
         dist.barrier(group=self.group)
         return self.full
 

@@ -162,3 +162,21 @@ def test_out_array_is_checked():
     for bad in (np.empty(5, dtype=np.float32), np.empty(4), np.empty(10)[::2], np.empty(6)):
         with pytest.raises(ValueError):
             D._out_array(bad, 5)
+
+
+@pytest.mark.parametrize("name", ["c1", "liver-desk", "prostate-desk"])
+def test_seeded_vector_pinned_to_reference_golden(golden, name):
+    """dg_seeded_vector (the headline bench's x) against the reference's own x: golden.json holds
+    checksum_bits(ddm::seeded_vector(cols, 42)) written by the reference (make_golden.py;
+    bench.cpp:31-36)."""
+    cols = {"c1": 4096, "liver-desk": 6800, "prostate-desk": 5090}[name]
+    assert f"{dg.checksum_bits(dg.seeded_vector(cols, 42)):016x}" == golden[name]["x_fnv"]
+
+
+@pytest.mark.parametrize("n,seed", [(40_000, 42), (196_608, 1000), (196_608, 1099), (1, 0), (0, 7)])
+def test_seeded_vector_equals_reference_at_config_sizes(ref, n, seed):
+    """C2's x and C4's optimisation-loop x_k = seeded_vector(196608, 1000 + k), bit for bit against
+    the reference compiled from its own sources (oracle/_ref)."""
+    a = dg.seeded_vector(n, seed)
+    b = ref.seeded_vector(n, seed)
+    assert np.array_equal(a.view(np.uint64), np.asarray(b, dtype=np.float64).view(np.uint64))

@@ -88,3 +88,35 @@ def test_ddm_upload_invalid_matrix_is_validation_failure(ref, tmp_path):
     open(p, "wb").write(bytes(b))
     assert ref.read_ddm_status(p) == 1 + dg.Errc.ValidationFailure
     assert _status(p) == 1 + dg.Errc.ValidationFailure
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("parts", [2, 5])
+def test_ddm_row_shards_read_only_their_ranges(ref, port, tmp_path, parts):
+    """A rank reads only its rows' byte ranges of the column and value sections (the layout is
+    fixed by the header, io.cpp:67-96): each shard's handle holds its shard only, reports its
+    place in the source matrix, and its d is bit-identical to the reference's rowchunk on the
+    file's matrix (read by ddm::read_ddm's writer counterpart) for those rows."""
+    m = ref.generate(prostate_desk())
+    p = str(tmp_path / "m.ddm")
+    ref.write_ddm(m, p)
+    x = port.seeded_vector(m.cols, 42)
+    want = ref.spmv_rowchunk(m, x, 32, 4)
+    b = dg.partition_rows(m.row_ptr, parts)
+    got = np.empty(m.rows)
+    for g in range(parts):
+        r0, r1 = int(b[g]), int(b[g + 1])
+        with dg.DoseEngine.from_ddm(p, row_begin=r0, row_end=r1) as e:
+            assert (e.info["row_begin"], e.info["row_end"], e.info["rows"]) == (r0, r1, r1 - r0)
+            assert e.info["nnz"] == int(m.row_ptr[r1] - m.row_ptr[r0])
+            # resident bytes are the shard's, not the file's
+            assert e.info["device_bytes"] < 1.5 * (e.info["nnz"] * 4 + 8 * (r1 - r0)) + (8 << 20)
+            got[r0:r1] = e.dose(x)
+            back = e.copy_rows(0, r1 - r0)
+            s0, s1 = int(m.row_ptr[r0]), int(m.row_ptr[r1])
+            assert np.array_equal(back.col_indices, m.col[s0:s1])
+            assert np.array_equal(back.values, m.values[s0:s1])
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+    with pytest.raises(dg.Error) as e:
+        dg.DoseEngine.from_ddm(p, row_begin=5, row_end=m.rows + 1)
+    assert e.value.code == dg.Errc.InvalidConfig
