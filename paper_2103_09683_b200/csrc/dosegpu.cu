@@ -277,6 +277,7 @@ int tile_buffers_of(int cfg, bool packed) {
 // owns is final before the tile kernel -- and the row-block completion signals -- start.
 template <class M, typename Acc>
 int launch_dense(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t s) {
+  if (h->dense_slices) return launch_dense_slices<Acc>(h, x, y, s);
   h->pdl_next = false;
   if (!h->n_dense_rows) return DG_OK;
   DG_CUDA(cudaMemsetAsync(h->d_dense_counter, 0, sizeof(uint32_t), s));
@@ -666,6 +667,9 @@ int dg_destroy(dg_handle* hh) {
   cudaFree(h->d_trace);
   cudaFree(h->d_dense_rows);
   cudaFree(h->d_dense_counter);
+  cudaFree(h->d_dslices);
+  cudaFree(h->d_dranges);
+  cudaFree(h->d_dsseg);
   cudaFree(h->d_col);
   cudaFree(h->d_val);
   cudaFree(h->d_packed);
@@ -713,8 +717,9 @@ int dg_dose(dg_handle* hh, const double* x, uint64_t x_len, double* y, uint32_t 
   // 16-byte aligned with a 16-byte multiple length and no window is replicated; otherwise x is
   // staged in the padded buffers (slot mode also needs the one-element-shifted copy, XSource).
   if (h->slot_tiles) DG_TRY(dg::recode_slots(h, false));
-  const bool x_direct = x_dev && !h->slot_tiles && (reinterpret_cast<uintptr_t>(x) % 16 == 0) &&
-                        (h->cols % 2 == 0);
+  // (dense slices read x[cols] for their neutral words: a staged +0.0 -- never the caller's x)
+  const bool x_direct = x_dev && !h->slot_tiles && !h->dense_slices &&
+                        (reinterpret_cast<uintptr_t>(x) % 16 == 0) && (h->cols % 2 == 0);
   const double* d_x = x_direct ? x : h->d_x;
   double* d_y = y_dev ? y : h->d_y;
   DG_CUDA(cudaEventRecord(h->ev[0], s));

@@ -84,6 +84,13 @@ struct Handle {
   uint64_t dense_min_len = 4096;  // C2: 2.69 ms (1024: 2.80); its 1/8 shard 0.394 ms (1024: 0.380)
   uint32_t* d_dense_rows = nullptr;  // longest first
   uint32_t* d_dense_counter = nullptr;
+  // dense rows over the slice layout (k_dense_slices, spmv_slices.cuh): Packed16 uploads with the
+  // slice stream; the rows are then not in the rest stream
+  bool dense_slices = false;
+  uint32_t* d_dslices = nullptr;   // lane-major 4-chunk blocks, one run per dense row
+  void* d_dranges = nullptr;       // WarpRange[n_dense_rows + 1]
+  void* d_dsseg = nullptr;         // SliceSeg[n_dense_rows]
+  uint64_t dense_chunks = 0;
   uint64_t n_dense_rows = 0, dense_nnz = 0;
   int dense_cfg = 0;  // DG_DENSE_CFG: (U, P) = (8, 4) default, 1: (16, 2), 2: (8, 8)
   bool pdl = true;       // DG_PDL: tile kernel as a programmatic dependent launch after k_dense
@@ -222,6 +229,8 @@ int build_slices(Handle* h);
 int decode_rows(const Handle* h, uint64_t r0, uint64_t r1, uint32_t* d_col, uint16_t* d_val);
 template <typename Acc>
 int launch_slices(Handle* h, const Acc* x, double* y, cudaStream_t s);
+template <typename Acc>
+int launch_dense_slices(Handle* h, const Acc* x, double* y, cudaStream_t s);
 // the upload's row pointer (rows in the reference's order)
 inline const uint64_t* orig_row_ptr(const Handle* h) { return h->d_row_ptr_orig ? h->d_row_ptr_orig : h->d_row_ptr; }
 int grid_for(uint64_t work_items, int threads, int max_blocks_per_sm = 8);

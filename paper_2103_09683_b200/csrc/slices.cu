@@ -147,6 +147,44 @@ __global__ void k_build_slices(M mat, const Tile* __restrict__ tiles, const Segm
   }
 }
 
+// Dense rows (k_dense_slices): one warp per row, the row's chunks in lane-major blocks from its
+// run's first chunk; positions past the row end are neutral words (column `cols`, value +0).
+__global__ void k_build_dense(Packed16 mat, const uint64_t* __restrict__ rp,
+                              const SliceSeg* __restrict__ sseg, const WarpRange* __restrict__ ranges,
+                              uint32_t n_rows, uint32_t* __restrict__ out, uint32_t neutral) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t n_gw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t k = gw; k < n_rows; k += n_gw) {
+    const uint32_t row = sseg[k].row;
+    const uint64_t s = rp[row], n = rp[row + 1] - s;
+    const uint64_t c0 = ranges[k].chunk, c1 = ranges[k + 1].chunk;
+    for (uint64_t c = c0; c < c1; ++c) {
+      const uint64_t rel = 32 * (c - c0) + lane;
+      out[slice_word(c, lane)] = rel < n ? mat.load(s + rel) : neutral;
+    }
+  }
+}
+
+__global__ void k_decode_dense(const uint32_t* __restrict__ w, const SliceSeg* __restrict__ sseg,
+                               const WarpRange* __restrict__ ranges, uint32_t n_rows,
+                               const uint64_t* __restrict__ rp, uint64_t r0, uint64_t r1, uint64_t b,
+                               uint32_t* __restrict__ col, uint16_t* __restrict__ val) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t n_gw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t k = gw; k < n_rows; k += n_gw) {
+    const uint32_t row = sseg[k].row;
+    if (row < r0 || row >= r1) continue;
+    const uint64_t s = rp[row], n = rp[row + 1] - s, c0 = ranges[k].chunk;
+    for (uint64_t rel = lane; rel < n; rel += 32) {
+      const uint32_t v = w[slice_word(c0 + rel / 32, lane)];
+      col[s + rel - b] = v >> 16;
+      val[s + rel - b] = static_cast<uint16_t>(v & 0xFFFFu);
+    }
+  }
+}
+
 // rows not owned by tiles (k_dense, the short-row bins): copied into a compacted stream of the
 // upload's format; rest_rp is a row pointer over it (tile rows have length 0)
 template <class M>
@@ -241,6 +279,39 @@ int build_slices(Handle* h) {
     DG_CUDA(cudaMemcpy(segs.data(), h->d_segs[0], segs.size() * sizeof(Segment), cudaMemcpyDeviceToHost));
     for (const Segment& s : segs) tile_row[s.row] = 1;
   }
+  // dense rows as one-segment runs (k_dense_slices): Packed16 (column field < 65536, so the
+  // neutral column `cols` fits), DG_DENSE_SLICES=0 keeps k_dense on the rest stream
+  h->dense_slices = h->packed && h->n_dense_rows > 0;
+  if (const char* ds = std::getenv("DG_DENSE_SLICES")) h->dense_slices = h->dense_slices && std::atoi(ds) != 0;
+  if (h->dense_slices) {
+    std::vector<uint32_t> drows(h->n_dense_rows);
+    DG_CUDA(cudaMemcpy(drows.data(), h->d_dense_rows, drows.size() * 4, cudaMemcpyDeviceToHost));
+    std::vector<WarpRange> R(drows.size() + 1);
+    std::vector<SliceSeg> S(drows.size());
+    uint64_t c = 0;
+    for (size_t k = 0; k < drows.size(); ++k) {
+      const uint32_t r = drows[k];
+      const uint32_t nch = static_cast<uint32_t>((rp[r + 1] - rp[r] + 31) / 32);
+      R[k] = {static_cast<uint32_t>(c), static_cast<uint32_t>(k)};
+      S[k] = {r, 0, nch, static_cast<uint32_t>(kSegFirst | kSegLast)};
+      c += (nch + kSliceBlock - 1) / kSliceBlock * kSliceBlock;
+      if (c > 0xFFFFFFFFull) return DG_ERR_UNSUPPORTED_FEATURE;
+      tile_row[r] = 1;  // not in the rest stream
+    }
+    R[drows.size()] = {static_cast<uint32_t>(c), static_cast<uint32_t>(drows.size())};
+    h->dense_chunks = c;
+    DG_CUDA(cudaMalloc(&h->d_dslices, std::max<uint64_t>(c * 32, 4) * 4));
+    DG_CUDA(cudaMalloc(&h->d_dranges, R.size() * sizeof(WarpRange)));
+    DG_CUDA(cudaMemcpy(h->d_dranges, R.data(), R.size() * sizeof(WarpRange), cudaMemcpyHostToDevice));
+    DG_CUDA(cudaMalloc(&h->d_dsseg, S.size() * sizeof(SliceSeg)));
+    DG_CUDA(cudaMemcpy(h->d_dsseg, S.data(), S.size() * sizeof(SliceSeg), cudaMemcpyHostToDevice));
+    h->plan_bytes += R.size() * sizeof(WarpRange) + S.size() * sizeof(SliceSeg);
+    k_build_dense<<<grid_for(32ull * drows.size(), 256, 8), 256>>>(
+        Packed16{h->d_packed}, h->d_row_ptr, static_cast<const SliceSeg*>(h->d_dsseg),
+        static_cast<const WarpRange*>(h->d_dranges), static_cast<uint32_t>(drows.size()), h->d_dslices,
+        static_cast<uint32_t>(h->cols) << 16);
+    DG_CUDA(cudaGetLastError());
+  }
   std::vector<uint64_t> rest_rp(h->rows + 1, 0);
   for (uint64_t r = 0; r < h->rows; ++r)
     rest_rp[r + 1] = rest_rp[r] + (tile_row[r] ? 0 : rp[r + 1] - rp[r]);
@@ -312,6 +383,10 @@ int decode_rows(const Handle* h, uint64_t r0, uint64_t r1, uint32_t* d_col, uint
         h->d_slices, static_cast<const Tile*>(h->d_tiles[0]), static_cast<const Segment*>(h->d_segs[0]),
         static_cast<const WarpRange*>(h->d_ranges), n_runs, h->slice_runs, h->rep_stride, b, e,
         d_col, d_val);
+  if (h->dense_slices)
+    k_decode_dense<<<grid_for(32ull * h->n_dense_rows, 256, 8), 256>>>(
+        h->d_dslices, static_cast<const SliceSeg*>(h->d_dsseg), static_cast<const WarpRange*>(h->d_dranges),
+        static_cast<uint32_t>(h->n_dense_rows), h->d_row_ptr_orig, r0, r1, b, d_col, d_val);
   if (h->rest_nnz) {
     const int st = dispatch_mat(h, [&](const auto& mat) {
       using M = std::decay_t<decltype(mat)>;
@@ -383,6 +458,28 @@ int launch_slices(Handle* h, const Acc* x, double* y, cudaStream_t s) {
   DG_CUDA(cudaGetLastError());
   return DG_OK;
 }
+template <typename Acc>
+int launch_dense_slices(Handle* h, const Acc* x, double* y, cudaStream_t s) {
+  h->pdl_next = false;
+  if (!h->n_dense_rows) return DG_OK;
+  DG_CUDA(cudaMemsetAsync(h->d_dense_counter, 0, sizeof(uint32_t), s));
+  // the tile kernel follows as a programmatic dependent launch unless something must sit between
+  // the two launches (per-launch profiling events, the row-block signals, the trace)
+  h->pdl_next = h->pdl && h->n_waves && !h->profiling && !h->signal_blocks && !h->d_trace;
+  if (h->pdl_next) DG_CUDA(cudaMemsetAsync(h->d_counters, 0, Handle::kMaxWaves * sizeof(uint32_t), s));
+  const int grid = h->pdl_next ? h->sm_count * 4 : grid_for(h->n_dense_rows * 32ull, 256, 8);
+  constexpr int kP = 4;
+  k_dense_slices<Acc, kP><<<grid, 256, 0, s>>>(
+      reinterpret_cast<const uint4*>(h->d_dslices), static_cast<const WarpRange*>(h->d_dranges),
+      static_cast<const SliceSeg*>(h->d_dsseg), static_cast<uint32_t>(h->n_dense_rows), x,
+      static_cast<uint32_t>(h->cols) << 16, h->d_dense_counter, y, h->gt);
+  h->post(s, "dense", h->n_dense_rows, h->dense_nnz);
+  DG_CUDA(cudaGetLastError());
+  return DG_OK;
+}
+template int launch_dense_slices<double>(Handle*, const double*, double*, cudaStream_t);
+template int launch_dense_slices<float>(Handle*, const float*, double*, cudaStream_t);
+
 template int launch_slices<double>(Handle*, const double*, double*, cudaStream_t);
 template int launch_slices<float>(Handle*, const float*, double*, cudaStream_t);
 

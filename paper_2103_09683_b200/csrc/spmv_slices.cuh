@@ -61,10 +61,23 @@ __device__ __forceinline__ uint4 ld_stream16(const uint4* p) {
 // of two blocks; an odd last block is paired with neutral words (`neutral`: the zero slot, value
 // +0).  Software pipeline: batch b + 1 is in flight in registers while batch b is gathered and
 // accumulated; lanes 0..7 prefetch the 8 lines of batch b + 1 + P into L2.
-template <typename Acc, int P, bool CARRY>
+// x sources of a run: the tile's shared-memory window (indexed by slot) or global x (dense rows:
+// their 32 lanes read consecutive columns, through L1 / L2)
+template <typename Acc>
+struct XSmem {
+  const Acc* base;
+  __device__ __forceinline__ Acc operator[](uint32_t i) const { return base[i]; }
+};
+template <typename Acc>
+struct XGlob {
+  const Acc* __restrict__ x;
+  __device__ __forceinline__ Acc operator[](uint32_t i) const { return __ldg(x + i); }
+};
+
+template <typename Acc, int P, bool CARRY, class XS = XSmem<Acc>>
 __device__ __forceinline__ void run_slice(const uint4* __restrict__ blocks, uint32_t c0, uint32_t nblk,
                                           const SliceSeg* __restrict__ sseg, uint32_t s0,
-                                          uint32_t s1, const Acc* xs, uint32_t neutral,
+                                          uint32_t s1, const XS xs, uint32_t neutral,
                                           const Carry<Acc>& carry, double* __restrict__ y,
                                           const GatherTargets& gt, uint32_t lane) {
   using Ops = AccOps<Acc>;
@@ -286,7 +299,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       const WarpRange r0 = ranges[static_cast<uint64_t>(t) * runs + k];
       const WarpRange r1 = ranges[static_cast<uint64_t>(t) * runs + k + 1];
       run_slice<Acc, P, CARRY>(blocks, r0.chunk, (r1.chunk - r0.chunk) / kSliceBlock, sseg, r0.seg,
-                               r1.seg, xbuf0 + b * wcap, (wcap - 1) << 16, carry, y, gt, lane);
+                               r1.seg, XSmem<Acc>{xbuf0 + b * wcap}, (wcap - 1) << 16, carry, y, gt,
+                               lane);
     }
     __syncwarp();
     if (lane == 0) {
@@ -316,6 +330,35 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     atomicAdd(&tr.cta[4ull * blockIdx.x + 2], static_cast<unsigned long long>(wait_cyc));
     atomicAdd(&tr.cta[4ull * blockIdx.x + 3], static_cast<unsigned long long>(clock64() - clk0));
     atomicMax(&tr.cta[4ull * blockIdx.x + 1], gtimer_ns());
+  }
+}
+
+// ---- dense rows over the slice layout ---------------------------------------------------------
+// The dense rows k_dense owns (>= 3/4 of their span, the longest rows) as runs of one segment
+// each, longest first, in the same lane-major 4-chunk blocks: each row starts on a 512-byte block
+// (its lane grid = the row's, lane0 0) and is padded to whole blocks with neutral words whose
+// column is `cols` (x[cols] is a staged +0.0).  Warps of persistent 8-warp CTAs pull rows
+// longest first and stream them with the tile kernel's run pipeline (two LDG.128 per lane per
+// 8-chunk batch, L2 prefetch P batches ahead); x comes from global memory through L1.
+template <typename Acc, int P>
+__global__ void __launch_bounds__(256)
+    k_dense_slices(const uint4* __restrict__ blocks, const WarpRange* __restrict__ ranges,
+                   const SliceSeg* __restrict__ sseg, uint32_t n_rows, const Acc* __restrict__ x,
+                   uint32_t neutral, uint32_t* __restrict__ counter, double* __restrict__ y,
+                   const __grid_constant__ GatherTargets gt) {
+  // programmatic dependent launch: the tile kernel that follows may take each SM as soon as this
+  // grid's CTAs there have exited (it touches other rows)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const uint32_t lane = threadIdx.x & 31;
+  const Carry<Acc> no_carry{nullptr};
+  for (;;) {
+    uint32_t k = 0;
+    if (lane == 0) k = atomicAdd(counter, 1u);
+    k = __shfl_sync(kFull, k, 0);
+    if (k >= n_rows) break;
+    const uint32_t c0 = ranges[k].chunk, c1 = ranges[k + 1].chunk;
+    run_slice<Acc, P, false>(blocks, c0, (c1 - c0) / kSliceBlock, sseg, k, k + 1, XGlob<Acc>{x},
+                             neutral, no_carry, y, gt, lane);
   }
 }
 
