@@ -483,7 +483,9 @@ def run_ours(args):
     tf = os.path.join(ROOT, "profiles", "dram_bytes_per_launch.json")
     if os.path.exists(tf) and world == 1 and not args.rows:  # profiled: the full 1-GPU workload
         try:
-            traffic = json.load(open(tf)).get(f"{args.config}:{args.accum}:{dom_name}")
+            tj = json.load(open(tf))
+            traffic = tj.get(f"{args.config}:{args.accum}:{dom_name}",
+                             tj.get(f"{args.config}:{args.accum}:{dom_name.split('[')[0]}"))
         except Exception:
             traffic = None
     info = engines[0].info

@@ -39,10 +39,11 @@ def launches(tag):
                                             1.0 if d["Metric Unit"] == "us" else 1e3)
             per.setdefault(name, []).append(v)
     dose = {k: v for k, v in per.items() if "gen_" not in k and "cub::" not in k and
-            "row_extents" not in k and "split_rows" not in k and "validate" not in k}
+            "row_extents" not in k and "split_rows" not in k and "validate" not in k and
+            "build_" not in k}
 
     def family(k):  # the bench runs the exact family, then the fp32 side line
-        return "fp32" if ("float" in k or "f32" in k) else "exact"
+        return "fp32" if ("float" in k or "f32" in k) else "exact"  # k_x_to_f32: fp32 x staging
 
     # one dose of a family = the sum of its kernels' average launch times
     step = collections.defaultdict(float)
@@ -69,7 +70,7 @@ def ncu(tag, family):
     hot = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "ncu_sass_hot.py"), rep,
                           "stall", "25"], capture_output=True, text=True).stdout
     cfg = "C4" if family == "c4" else "C2"
-    text = (f"# {tag}: ncu --set full --clock-control none, dose kernels k_tiles (+ k_dense) ({cfg}, {family})\n"
+    text = (f"# {tag}: ncu --set full --clock-control none, dose kernels k_slices / k_tiles (+ k_dense) ({cfg}, {family})\n"
             + summ + "\n# hottest SASS by warp-stall samples (addr, executed, samples, instr)\n" + hot)
     open(os.path.join(PROF, f"{tag}_ncu_{family}.txt"), "w").write(text)
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
@@ -87,7 +88,7 @@ def ncu(tag, family):
     out = {}
     for v in r[2:]:
         name = v[hdr.index("Kernel Name")] if "Kernel Name" in hdr else ""
-        key = "dense" if "k_dense" in name else "tiles"
+        key = "dense" if "k_dense" in name else ("slices" if "k_slices" in name else "tiles")
         if key not in out:
             out[key] = get(v, "dram__bytes_read.sum") + get(v, "dram__bytes_write.sum")
     return out
@@ -106,8 +107,8 @@ def main():
         t = ncu(tag, fam)
         if t is None:
             continue
-        for k, b in t.items():
-            traffic[f"{prefix}:{tiles if k == 'tiles' else 'dense'}"] = int(b)
+        for k, b in t.items():  # slices: bench.py looks the name up without its "[...]" suffix
+            traffic[f"{prefix}:{tiles if k == 'tiles' else k}"] = int(b)
             print(fam, k, "dram bytes per launch", b)
     json.dump(traffic, open(tf, "w"), indent=1, sort_keys=True)
 
