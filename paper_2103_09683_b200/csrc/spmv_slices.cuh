@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
              const __grid_constant__ GatherTargets gt, TileTrace tr) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   // full[b]: the window of buffer b has landed (TMA complete_tx); empty[b]: every warp has left
-  // buffer b (WARPS arrivals) -- the refill of b waits on it, so the window's readers are ordered
+  // buffer b (WARPS x 32 arrivals) -- the refill of b waits on it, so the window's readers are ordered
   // before its next TMA overwrite by barrier operations (visible to compute-sanitizer racecheck)
   __shared__ __align__(8) uint64_t full[NB], empty[NB];
   __shared__ uint32_t tile_of[NB], done[NB], run_next[NB];
@@ -206,66 +206,74 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   const uint32_t lane = threadIdx.x & 31;
   const Acc* __restrict__ x = xsrc.x;
 
-  auto refill = [&](int b) {
-    const uint32_t t = atomicAdd(counter, 1u);
-    tile_of[b] = t;
-    done[b] = 0;
-    run_next[b] = 0;
+  __shared__ uint32_t blk_of[NB];
+  // warp-collective: put tile t into buffer b -- stage its x window by TMA (lane 0) and prefetch
+  // the first 2 KB of each of its runs plus its segment descriptors into L2 (the lanes in
+  // parallel), so the warps start the tile's runs on L2 hits.  The tile_of / done / run_next
+  // stores precede lane 0's arrive on full[b] (release), which every reader acquires.
+  auto refill = [&](int b, uint32_t t) {
     if (t < n_tiles) {
       const Tile T = tiles[t];
-      if (tr.cta) {
-        tr.tile[3ull * t] = gtimer_ns();
-        tr.tile[3ull * t + 2] = blockIdx.x | (static_cast<unsigned long long>(T.seg1 - T.seg0) << 16);
+      if (lane == 0) {
+        tile_of[b] = t;
+        blk_of[b] = T.blk;
+        done[b] = 0;
+        run_next[b] = 0;
+        if (tr.cta) {
+          tr.tile[3ull * t] = gtimer_ns();
+          tr.tile[3ull * t + 2] = blockIdx.x | (static_cast<unsigned long long>(T.seg1 - T.seg0) << 16);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        char* const dst0 = reinterpret_cast<char*>(xbuf0 + b * wcap);
+        constexpr uint32_t kAl = 16 / sizeof(Acc);
+        uint32_t total = 0;
+        const uint32_t nrep = T.nrep;
+        for (uint32_t r = 0; r < nrep; ++r)
+          total += (T.xlen + rep_shift(r) + kAl - 1) / kAl * kAl * static_cast<uint32_t>(sizeof(Acc));
+        mbar_arrive_expect_tx(&full[b], total);
+        for (uint32_t r = 0; r < nrep; ++r) {
+          const uint32_t sh = rep_shift(r);
+          const uint32_t bytes = (T.xlen + sh + kAl - 1) / kAl * kAl * static_cast<uint32_t>(sizeof(Acc));
+          const Acc* base = (sh % kAl) ? xsrc.x1 : x;
+          const char* src = reinterpret_cast<const char*>(base + T.xlo) - sh * sizeof(Acc);
+          char* dst = dst0 + static_cast<size_t>(r) * xsrc.rep_stride * sizeof(Acc);
+          for (uint32_t off = 0; off < bytes; off += 32768u)
+            tma_load_1d(dst + off, src + off, min(32768u, bytes - off), &full[b]);
+        }
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      char* const dst0 = reinterpret_cast<char*>(xbuf0 + b * wcap);
-      constexpr uint32_t kAl = 16 / sizeof(Acc);
-      uint32_t total = 0;
-      const uint32_t nrep = T.nrep;
-      for (uint32_t r = 0; r < nrep; ++r)
-        total += (T.xlen + rep_shift(r) + kAl - 1) / kAl * kAl * static_cast<uint32_t>(sizeof(Acc));
-      mbar_arrive_expect_tx(&full[b], total);
-      for (uint32_t r = 0; r < nrep; ++r) {
-        const uint32_t sh = rep_shift(r);
-        const uint32_t bytes = (T.xlen + sh + kAl - 1) / kAl * kAl * static_cast<uint32_t>(sizeof(Acc));
-        const Acc* base = (sh % kAl) ? xsrc.x1 : x;
-        const char* src = reinterpret_cast<const char*>(base + T.xlo) - sh * sizeof(Acc);
-        char* dst = dst0 + static_cast<size_t>(r) * xsrc.rep_stride * sizeof(Acc);
-        for (uint32_t off = 0; off < bytes; off += 32768u)
-          tma_load_1d(dst + off, src + off, min(32768u, bytes - off), &full[b]);
-      }
-      // the first 2 KB of every run and the tile's segment descriptors into L2: the warps
-      // start the tile's runs on L2 hits
       const WarpRange* R = ranges + static_cast<uint64_t>(t) * runs;
-      for (uint32_t w = 0; w < runs; ++w) {
+      for (uint32_t w = lane; w < runs; w += 32) {
         const uint32_t c = R[w].chunk, ce = R[w + 1].chunk;
         if (ce > c)
           asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(blocks + static_cast<uint64_t>(c / 4) * 32),
-                       "r"(min(2048u, (ce - c) * 128u))
-                       : "memory");
+                       "r"(min(2048u, (ce - c) * 128u)));
       }
-      const uint64_t sb = reinterpret_cast<uint64_t>(sseg + R[0].seg) & ~15ull;
-      const uint64_t se = reinterpret_cast<uint64_t>(sseg + R[runs].seg);
-      if (se > sb)
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sb),
-                     "r"(static_cast<uint32_t>(se - sb))
-                     : "memory");
-    } else {
-      mbar_arrive(&full[b]);
+      if (lane == 0) {
+        const uint64_t sb = reinterpret_cast<uint64_t>(sseg + R[0].seg) & ~15ull;
+        const uint64_t se = reinterpret_cast<uint64_t>(sseg + R[runs].seg);
+        if (se > sb)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sb),
+                       "r"(static_cast<uint32_t>(se - sb)));
+      }
+    } else if (lane == 0) {
+      tile_of[b] = t;
+      mbar_arrive(&full[b]);  // terminal: completes the phase with tile_of[b] >= n_tiles
     }
+    __syncwarp();
   };
 
   if (threadIdx.x < NB) xbuf0[threadIdx.x * wcap + wcap - 1] = Acc(0);  // zero slots
   if (threadIdx.x == 0)
     for (int i = 0; i < NB; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], WARPS);
+      mbar_init(&empty[i], WARPS * 32);  // every thread arrives
     }
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
-  if (threadIdx.x == 0)
-    for (int i = 0; i < NB; ++i) refill(i);
-  __syncthreads();
+  // the first NB tiles are static (CTA i: tiles i, i + grid, ...; no claim latency at the start),
+  // staged by warps 0 .. NB-1 in parallel; later tiles are claimed in order from the counter
+  const uint32_t warp = threadIdx.x / 32;
+  if (warp < NB) refill(static_cast<int>(warp), blockIdx.x + warp * gridDim.x);
 
   uint32_t phases = 0;
   int b = 0;
@@ -305,23 +313,29 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     __syncwarp();
     if (lane == 0) {
       if (sig.left) __threadfence(); else __threadfence_block();
-      mbar_arrive(&empty[b]);  // release: this warp's reads of buffer b are done
-      if (atomicAdd(&done[b], 1u) == WARPS - 1) {  // the last warp to leave refills b
-        mbar_wait(&empty[b], ((phases >> b) & 1u) ^ 1u);  // acquire every warp's release
-        const Tile T = tiles[t];
-        if (tr.cta) tr.tile[3ull * t + 1] = gtimer_ns();
-        if (sig.left && T.blk != kNoBlock) {
-          __threadfence();
-          if (atomicSub(&sig.left[T.blk], 1u) == 1u) {
-            __threadfence();
-            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(sig.flag + T.blk),
-                         "r"(sig.epoch)
-                         : "memory");
-          }
-        }
-        refill(b);
-      }
     }
+    __syncwarp();
+    // release: every lane's reads of buffer b (the window, tile_of[b]) are done -- each thread
+    // arrives for itself, so the ordering does not rest on __syncwarp (racecheck models it so)
+    mbar_arrive(&empty[b]);
+    uint32_t next = 0xFFFFFFFFu;  // the last warp to leave refills b with the next claimed tile
+    if (lane == 0 && atomicAdd(&done[b], 1u) == WARPS - 1) {
+      mbar_wait(&empty[b], ((phases >> b) & 1u) ^ 1u);  // acquire every warp's release
+      const uint32_t blk = blk_of[b];
+      if (tr.cta) tr.tile[3ull * t + 1] = gtimer_ns();
+      if (sig.left && blk != kNoBlock) {
+        __threadfence();
+        if (atomicSub(&sig.left[blk], 1u) == 1u) {
+          __threadfence();
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(sig.flag + blk),
+                       "r"(sig.epoch)
+                       : "memory");
+        }
+      }
+      next = atomicAdd(counter, 1u) + NB * gridDim.x;
+    }
+    next = __shfl_sync(kFull, next, 0);
+    if (next != 0xFFFFFFFFu) refill(b, next);
     __syncwarp();
     b = b + 1 == NB ? 0 : b + 1;
   }

@@ -655,7 +655,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < NB; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], WARPS);
+      mbar_init(&empty[i], WARPS * 32);  // every thread arrives
     }
   }
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -700,7 +700,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     if (lane == 0) {
       // this warp's reads of buffer b (and, when signalling, its d stores) happen before the count
       if (sig.left) __threadfence(); else __threadfence_block();
-      mbar_arrive(&empty[b]);  // release: this warp's reads of buffer b are done
+    }
+    __syncwarp();
+    mbar_arrive(&empty[b]);  // release: every lane's reads of buffer b are done (each arrives)
+    if (lane == 0) {
       if (atomicAdd(&done[b], 1u) == WARPS - 1) {  // the tile is finished
         mbar_wait(&empty[b], ((phases >> b) & 1u) ^ 1u);  // acquire every warp's release
         if (tr.cta) tr.tile[3ull * t + 1] = gtimer_ns();

@@ -9,5 +9,5 @@ for r in $(seq ${REPS:-3}); do
     echo "=== [$r] $v $ARGS"; env $v timeout 240 python bench.py --no-cpu-baseline $ARGS | q
   done
 done
-} > gpurun_out/ab_alt.txt 2>&1
-cat gpurun_out/ab_alt.txt
+} > gpurun_out/${OUT:-ab_alt}.txt 2>&1
+cat gpurun_out/${OUT:-ab_alt}.txt

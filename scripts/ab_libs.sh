@@ -10,6 +10,6 @@ for r in $(seq ${REPS:-3}); do
     echo "=== [$r] $v $ARGS"; env ${ENVS} timeout 240 python bench.py --no-cpu-baseline $ARGS | q
   done
 done
-} > gpurun_out/ab_libs.txt 2>&1
+} > gpurun_out/${OUT:-ab_libs}.txt 2>&1
 cp /tmp/lib_current.so paper_2103_09683_b200/libdosegpu.so
-cat gpurun_out/ab_libs.txt
+cat gpurun_out/${OUT:-ab_libs}.txt
