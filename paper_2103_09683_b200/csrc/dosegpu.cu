@@ -277,8 +277,9 @@ int tile_buffers_of(int cfg, bool packed) {
 // owns is final before the tile kernel -- and the row-block completion signals -- start.
 template <class M, typename Acc>
 int launch_dense(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t s) {
-  if (h->dense_slices) return launch_dense_slices<Acc>(h, x, y, s);
   h->pdl_next = false;
+  DG_TRY(launch_values<Acc>(h, x, y, s, h->n_dense_rows == 0));  // the contiguous rows first
+  if (h->dense_slices) return launch_dense_slices<Acc>(h, x, y, s);
   if (!h->n_dense_rows) return DG_OK;
   DG_CUDA(cudaMemsetAsync(h->d_dense_counter, 0, sizeof(uint32_t), s));
   // The tile kernel follows as a programmatic dependent launch (it may start on SMs k_dense has
@@ -670,6 +671,9 @@ int dg_destroy(dg_handle* hh) {
   cudaFree(h->d_dslices);
   cudaFree(h->d_dranges);
   cudaFree(h->d_dsseg);
+  cudaFree(h->d_vrows);
+  cudaFree(h->d_vstream);
+  cudaFree(h->d_value_counter);
   cudaFree(h->d_col);
   cudaFree(h->d_val);
   cudaFree(h->d_packed);
@@ -718,7 +722,7 @@ int dg_dose(dg_handle* hh, const double* x, uint64_t x_len, double* y, uint32_t 
   // staged in the padded buffers (slot mode also needs the one-element-shifted copy, XSource).
   if (h->slot_tiles) DG_TRY(dg::recode_slots(h, false));
   // (dense slices read x[cols] for their neutral words: a staged +0.0 -- never the caller's x)
-  const bool x_direct = x_dev && !h->slot_tiles && !h->dense_slices &&
+  const bool x_direct = x_dev && !h->slot_tiles && !h->dense_slices && !h->n_value_rows &&
                         (reinterpret_cast<uintptr_t>(x) % 16 == 0) && (h->cols % 2 == 0);
   const double* d_x = x_direct ? x : h->d_x;
   double* d_y = y_dev ? y : h->d_y;

@@ -92,6 +92,15 @@ struct Handle {
   void* d_dsseg = nullptr;         // SliceSeg[n_dense_rows]
   uint64_t dense_chunks = 0;
   uint64_t n_dense_rows = 0, dense_nnz = 0;
+  // contiguous rows (columns lo .. lo + len - 1: every dense row of the reference generator's
+  // profiles at len >= its locality window) at least dense_min_len long, with the slice stream:
+  // streamed as binary16 values only (k_dense_values, spmv_slices.cuh) -- the column of position
+  // p is lo + p, so 2 bytes per nonzero instead of 4; not in the rest stream
+  std::vector<uint8_t> dense_contig;  // plan -> build_slices: per dense row (longest first)
+  uint64_t n_value_rows = 0, value_nnz = 0, value_blocks = 0;
+  void* d_vrows = nullptr;            // DenseRow[n_value_rows], longest first
+  uint16_t* d_vstream = nullptr;      // lane-major 8-chunk blocks of binary16 values
+  uint32_t* d_value_counter = nullptr;
   int dense_cfg = 0;  // DG_DENSE_CFG: (U, P) = (8, 4) default, 1: (16, 2), 2: (8, 8)
   bool pdl = true;       // DG_PDL: tile kernel as a programmatic dependent launch after k_dense
   bool pdl_next = false; // (this dose: the next launch is that dependent launch)
@@ -174,6 +183,7 @@ struct Handle {
       for (int b = 0; b < kNumBins; ++b) n += bin_count[b] ? 1 : 0;
       for (uint32_t w = 0; w < n_launch_lists(); ++w) n += wave_tiles[w] ? 1 : 0;
       n += n_dense_rows ? 1 : 0;
+      n += n_value_rows ? 1 : 0;
     } else {
       n += bin_count[kBinGeneral] ? 1 : 0;
     }
@@ -231,6 +241,8 @@ template <typename Acc>
 int launch_slices(Handle* h, const Acc* x, double* y, cudaStream_t s);
 template <typename Acc>
 int launch_dense_slices(Handle* h, const Acc* x, double* y, cudaStream_t s);
+template <typename Acc>
+int launch_values(Handle* h, const Acc* x, double* y, cudaStream_t s, bool last);
 // the upload's row pointer (rows in the reference's order)
 inline const uint64_t* orig_row_ptr(const Handle* h) { return h->d_row_ptr_orig ? h->d_row_ptr_orig : h->d_row_ptr; }
 int grid_for(uint64_t work_items, int threads, int max_blocks_per_sm = 8);

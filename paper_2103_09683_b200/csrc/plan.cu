@@ -190,6 +190,14 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
   }
   // (the slice stream has no global-x segments: every dense row wider than a window is k_dense's)
   h->dense_kernel = h->dense_mode != 0 && (dense_all || 100 * wide_dense >= h->nnz || (slices && wide_dense));
+  // contiguous rows >= dense_min_len go to k_dense_values whenever the slice stream is planned
+  // (binary16 values under lane width 32): their column words are implied, half the bytes
+  auto contiguous = [&](uint64_t r) {
+    return slices && h->dense_mode != 0 && lens[r] >= h->dense_min_len && lens[r] > h->short_max &&
+           static_cast<uint64_t>(ext[r].y) - ext[r].x + 1 == lens[r];
+  };
+  if (!h->dense_kernel)
+    for (uint64_t r = 0; r < rows && !h->dense_kernel; ++r) h->dense_kernel = contiguous(r);
   std::vector<std::vector<HostSeg>> waves(1);
   std::vector<HostSeg> global_x;
   std::vector<uint32_t> wide, dense_rows;
@@ -199,8 +207,8 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     const uint64_t span = static_cast<uint64_t>(c1) - c0 + 1;
     const uint16_t whole = static_cast<uint16_t>(kSegFirst | kSegLast);
     const bool dense = 4 * lens[r] >= 3 * span;
-    if (h->dense_kernel && dense && lens[r] >= h->dense_min_len &&
-        (dense_all || span > ws)) {  // k_dense
+    if ((h->dense_kernel && dense && lens[r] >= h->dense_min_len && (dense_all || span > ws)) ||
+        contiguous(r)) {  // k_dense / k_dense_values
       dense_rows.push_back(static_cast<uint32_t>(r));
       h->dense_nnz += lens[r];
       continue;
@@ -221,6 +229,8 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
   if (!dense_rows.empty()) {  // longest first: the pool ends with the shortest rows
     std::stable_sort(dense_rows.begin(), dense_rows.end(),
                      [&](uint32_t a, uint32_t b) { return lens[a] > lens[b]; });
+    h->dense_contig.resize(dense_rows.size());
+    for (size_t i = 0; i < dense_rows.size(); ++i) h->dense_contig[i] = contiguous(dense_rows[i]);
     DG_CUDA(cudaMalloc(&h->d_dense_rows, dense_rows.size() * sizeof(uint32_t)));
     DG_CUDA(cudaMemcpy(h->d_dense_rows, dense_rows.data(), dense_rows.size() * sizeof(uint32_t),
                        cudaMemcpyHostToDevice));

@@ -185,6 +185,48 @@ __global__ void k_decode_dense(const uint32_t* __restrict__ w, const SliceSeg* _
   }
 }
 
+// Contiguous rows as values only (k_dense_values): one warp per row, which also records the row's
+// first column in its descriptor.
+template <class M>
+__global__ void k_build_values(M mat, const uint64_t* __restrict__ rp, DenseRow* __restrict__ rows,
+                               uint32_t n_rows, uint16_t* __restrict__ out) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t n_gw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t k = gw; k < n_rows; k += n_gw) {
+    const DenseRow R = rows[k];
+    const uint64_t s = rp[R.row];
+    if (lane == 0) rows[k].lo = static_cast<uint32_t>(mat.col_at(s));
+    const uint32_t nblk = ((R.len + 31) / 32 + kValueChunks - 1) / kValueChunks;
+    for (uint32_t b = 0; b < nblk; ++b)
+      for (uint32_t i = 0; i < kValueChunks; ++i) {
+        const uint32_t pos = 32 * (kValueChunks * b + i) + lane;
+        out[(static_cast<uint64_t>(R.blk) + b) * (32 * kValueChunks) + kValueChunks * lane + i] =
+            pos < R.len ? static_cast<uint16_t>(M::v_of(mat.load(s + pos))) : uint16_t(0);
+      }
+  }
+}
+
+__global__ void k_decode_values(const uint16_t* __restrict__ vs, const DenseRow* __restrict__ rows,
+                                uint32_t n_rows, const uint64_t* __restrict__ rp, uint64_t r0,
+                                uint64_t r1, uint64_t b, uint32_t* __restrict__ col,
+                                uint16_t* __restrict__ val) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t n_gw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t k = gw; k < n_rows; k += n_gw) {
+    const DenseRow R = rows[k];
+    if (R.row < r0 || R.row >= r1) continue;
+    const uint64_t s = rp[R.row];
+    for (uint32_t rel = lane; rel < R.len; rel += 32) {
+      const uint32_t c = rel / 32;
+      col[s + rel - b] = R.lo + rel;
+      val[s + rel - b] = vs[(static_cast<uint64_t>(R.blk) + c / kValueChunks) * (32 * kValueChunks) +
+                            kValueChunks * lane + c % kValueChunks];
+    }
+  }
+}
+
 // rows not owned by tiles (k_dense, the short-row bins): copied into a compacted stream of the
 // upload's format; rest_rp is a row pointer over it (tile rows have length 0)
 template <class M>
@@ -278,6 +320,51 @@ int build_slices(Handle* h) {
     std::vector<Segment> segs(h->n_segments);
     DG_CUDA(cudaMemcpy(segs.data(), h->d_segs[0], segs.size() * sizeof(Segment), cudaMemcpyDeviceToHost));
     for (const Segment& s : segs) tile_row[s.row] = 1;
+  }
+  // contiguous dense rows as values only (k_dense_values); the others stay k_dense's
+  if (h->n_dense_rows && h->dense_contig.size() == h->n_dense_rows) {
+    std::vector<uint32_t> drows(h->n_dense_rows), vrows, wrows;
+    DG_CUDA(cudaMemcpy(drows.data(), h->d_dense_rows, drows.size() * 4, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < drows.size(); ++i) (h->dense_contig[i] ? vrows : wrows).push_back(drows[i]);
+    if (!vrows.empty()) {
+      std::vector<DenseRow> V(vrows.size());
+      uint64_t blk = 0, vnnz = 0;
+      for (size_t k = 0; k < vrows.size(); ++k) {
+        const uint32_t r = vrows[k];
+        const uint64_t len = rp[r + 1] - rp[r];
+        V[k] = {r, 0, static_cast<uint32_t>(len), static_cast<uint32_t>(blk)};
+        blk += ((len + 31) / 32 + kValueChunks - 1) / kValueChunks;
+        if (blk > 0xFFFFFFFFull) return DG_ERR_UNSUPPORTED_FEATURE;
+        vnnz += len;
+        tile_row[r] = 1;  // not in the rest stream
+      }
+      h->n_value_rows = vrows.size();
+      h->value_nnz = vnnz;
+      h->value_blocks = blk;
+      DG_CUDA(cudaMalloc(&h->d_vrows, V.size() * sizeof(DenseRow)));
+      DG_CUDA(cudaMemcpy(h->d_vrows, V.data(), V.size() * sizeof(DenseRow), cudaMemcpyHostToDevice));
+      DG_CUDA(cudaMalloc(&h->d_vstream, std::max<uint64_t>(blk, 1) * 32 * kValueChunks * 2));
+      DG_CUDA(cudaMalloc(&h->d_value_counter, sizeof(uint32_t)));
+      h->plan_bytes += V.size() * sizeof(DenseRow);
+      const int st = dispatch_mat(h, [&](const auto& mat) {
+        using M = std::decay_t<decltype(mat)>;
+        if constexpr (std::is_same_v<typename M::Val, uint16_t>) {
+          k_build_values<M><<<grid_for(32ull * vrows.size(), 256, 8), 256>>>(
+              mat, h->d_row_ptr, static_cast<DenseRow*>(h->d_vrows), static_cast<uint32_t>(vrows.size()),
+              h->d_vstream);
+          return DG_OK;
+        } else {
+          return DG_ERR_UNSUPPORTED_FEATURE;
+        }
+      });
+      if (st) return st;
+      DG_CUDA(cudaGetLastError());
+      // the word rows stay in d_dense_rows (longest first)
+      h->n_dense_rows = wrows.size();
+      h->dense_nnz -= vnnz;
+      if (!wrows.empty())
+        DG_CUDA(cudaMemcpy(h->d_dense_rows, wrows.data(), wrows.size() * 4, cudaMemcpyHostToDevice));
+    }
   }
   // dense rows as one-segment runs (k_dense_slices): Packed16 (column field < 65536, so the
   // neutral column `cols` fits), DG_DENSE_SLICES=0 keeps k_dense on the rest stream
@@ -383,6 +470,10 @@ int decode_rows(const Handle* h, uint64_t r0, uint64_t r1, uint32_t* d_col, uint
         h->d_slices, static_cast<const Tile*>(h->d_tiles[0]), static_cast<const Segment*>(h->d_segs[0]),
         static_cast<const WarpRange*>(h->d_ranges), n_runs, h->slice_runs, h->rep_stride, b, e,
         d_col, d_val);
+  if (h->n_value_rows)
+    k_decode_values<<<grid_for(32ull * h->n_value_rows, 256, 8), 256>>>(
+        h->d_vstream, static_cast<const DenseRow*>(h->d_vrows), static_cast<uint32_t>(h->n_value_rows),
+        h->d_row_ptr_orig, r0, r1, b, d_col, d_val);
   if (h->dense_slices)
     k_decode_dense<<<grid_for(32ull * h->n_dense_rows, 256, 8), 256>>>(
         h->d_dslices, static_cast<const SliceSeg*>(h->d_dsseg), static_cast<const WarpRange*>(h->d_dranges),
@@ -458,10 +549,29 @@ int launch_slices(Handle* h, const Acc* x, double* y, cudaStream_t s) {
   DG_CUDA(cudaGetLastError());
   return DG_OK;
 }
+// the contiguous rows (k_dense_values); `last`: no other dense launch follows, so the tile
+// kernel may follow it as a programmatic dependent launch
+template <typename Acc>
+int launch_values(Handle* h, const Acc* x, double* y, cudaStream_t s, bool last) {
+  if (!h->n_value_rows) return DG_OK;
+  DG_CUDA(cudaMemsetAsync(h->d_value_counter, 0, sizeof(uint32_t), s));
+  h->pdl_next = last && h->pdl && h->n_waves && !h->profiling && !h->signal_blocks && !h->d_trace;
+  if (h->pdl_next) DG_CUDA(cudaMemsetAsync(h->d_counters, 0, Handle::kMaxWaves * sizeof(uint32_t), s));
+  const int grid = h->pdl_next ? h->sm_count * 4 : grid_for(h->n_value_rows * 32ull, 256, 8);
+  k_dense_values<Acc, 2><<<grid, 256, 0, s>>>(
+      reinterpret_cast<const uint4*>(h->d_vstream), static_cast<const DenseRow*>(h->d_vrows),
+      static_cast<uint32_t>(h->n_value_rows), x, static_cast<uint32_t>(h->cols), h->d_value_counter, y, h->gt);
+  h->post(s, "dense_values", h->n_value_rows, h->value_nnz);
+  DG_CUDA(cudaGetLastError());
+  return DG_OK;
+}
+template int launch_values<double>(Handle*, const double*, double*, cudaStream_t, bool);
+template int launch_values<float>(Handle*, const float*, double*, cudaStream_t, bool);
+
 template <typename Acc>
 int launch_dense_slices(Handle* h, const Acc* x, double* y, cudaStream_t s) {
-  h->pdl_next = false;
   if (!h->n_dense_rows) return DG_OK;
+  h->pdl_next = false;
   DG_CUDA(cudaMemsetAsync(h->d_dense_counter, 0, sizeof(uint32_t), s));
   // the tile kernel follows as a programmatic dependent launch unless something must sit between
   // the two launches (per-launch profiling events, the row-block signals, the trace)

@@ -376,6 +376,91 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ---- contiguous rows as values only ----------------------------------------------------------
+// A row whose columns are lo, lo + 1, ..., lo + len - 1 needs no column words: position p reads
+// x[lo + p].  k_dense_values streams such rows as binary16 values alone -- 2 bytes per nonzero
+// instead of 4 -- in lane-major 8-chunk blocks (512 bytes: lane l's 16 bytes are its 8 values of
+// chunks 8b .. 8b + 7, positions 32 c + l), each row starting on a block and padded to whole
+// blocks with +0 values.  Lane l adds the same products in the same order from +0.0 as the
+// reference's lane l (spmv.cpp:58-63); padding positions read x[zero_col] (a staged +0.0, never
+// the caller's x: +0 * Inf would be NaN), so they add +0.0 exactly.  Warps of persistent 8-warp
+// CTAs pull rows longest first; a batch is 16 chunks (two LDG.128 per lane), the next batch in
+// flight in registers and an L2 prefetch stream P batches ahead; x comes through L1 (32 lanes
+// read 32 consecutive elements per chunk).
+struct DenseRow {
+  uint32_t row;
+  uint32_t lo;   // first column (written by k_build_values)
+  uint32_t len;
+  uint32_t blk;  // first 512-byte block of the row in the value stream
+};
+constexpr int kValueChunks = 8;  // chunks per 512-byte value block
+
+template <typename Acc, int P>
+__global__ void __launch_bounds__(256)
+    k_dense_values(const uint4* __restrict__ vs, const DenseRow* __restrict__ rows, uint32_t n_rows,
+                   const Acc* __restrict__ x, uint32_t zero_col, uint32_t* __restrict__ counter,
+                   double* __restrict__ y, const __grid_constant__ GatherTargets gt) {
+  // programmatic dependent launch: the kernel that follows may take each SM as soon as this
+  // grid's CTAs there have exited (it touches other rows)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  using Ops = AccOps<Acc>;
+  const uint32_t lane = threadIdx.x & 31;
+  for (;;) {
+    uint32_t k = 0;
+    if (lane == 0) k = atomicAdd(counter, 1u);
+    k = __shfl_sync(kFull, k, 0);
+    if (k >= n_rows) break;
+    const DenseRow R = rows[k];
+    const uint32_t nblk = ((R.len + 31) / 32 + kValueChunks - 1) / kValueChunks;
+    const uint32_t nb = (nblk + 1) / 2;  // batches of two blocks
+    const uint4* p = vs + static_cast<uint64_t>(R.blk) * 32 + lane;
+    const Acc* xr = x + R.lo;
+    const uint4 zero = make_uint4(0, 0, 0, 0);
+    uint4 a0 = ld_stream16(p), a1 = nblk > 1 ? ld_stream16(p + 32) : zero, b0 = zero, b1 = zero;
+    if constexpr (P > 0) {
+#pragma unroll
+      for (int j = 1; j <= P; ++j)
+        if (lane < 8 && 2 * j + (lane >= 4 ? 1u : 0u) < nblk)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(p - lane + 64 * j) + 128 * lane));
+    }
+    Acc acc = Acc(0);
+    for (uint32_t bi = 0; bi < nb; ++bi) {
+      if (bi + 1 < nb) {
+        b0 = ld_stream16(p + 64);
+        b1 = 2 * bi + 3 < nblk ? ld_stream16(p + 96) : zero;
+      }
+      if constexpr (P > 0)
+        if (lane < 8 && 2 * (bi + 1 + P) + (lane >= 4 ? 1u : 0u) < nblk)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(p - lane + 64 * (1 + P)) + 128 * lane));
+      const uint32_t w[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const uint32_t pos0 = bi * (2 * kValueChunks * 32) + lane;
+      Acc xv[2 * kValueChunks];
+      if (pos0 + (2 * kValueChunks - 1) * 32 < R.len) {  // interior batch
+#pragma unroll
+        for (int c = 0; c < 2 * kValueChunks; ++c) xv[c] = __ldg(xr + pos0 + 32 * c);
+      } else {  // the row's last batch: positions past the end read the staged +0.0
+#pragma unroll
+        for (int c = 0; c < 2 * kValueChunks; ++c) {
+          const uint32_t pos = pos0 + 32 * c;
+          xv[c] = __ldg(pos < R.len ? xr + pos : x + zero_col);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 2 * kValueChunks; ++c)
+        acc = Ops::add(acc, Ops::prod(static_cast<uint16_t>(w[c / 2] >> (16 * (c & 1))), xv[c]));
+      a0 = b0;
+      a1 = b1;
+      p += 64;
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off /= 2) acc = Ops::add(acc, __shfl_down_sync(kFull, acc, off));
+    if (lane == 0) {
+      y[R.row] = static_cast<double>(acc);
+      gt.store(R.row, static_cast<double>(acc));
+    }
+  }
+}
+
 // word index of (chunk c, lane l) in the lane-major 4-chunk blocks
 __host__ __device__ __forceinline__ uint64_t slice_word(uint64_t c, uint32_t l) {
   return (c >> 2) * 128 + 4 * l + (c & 3);

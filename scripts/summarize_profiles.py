@@ -88,7 +88,8 @@ def ncu(tag, family):
     out = {}
     for v in r[2:]:
         name = v[hdr.index("Kernel Name")] if "Kernel Name" in hdr else ""
-        key = "dense" if "k_dense" in name else ("slices" if "k_slices" in name else "tiles")
+        key = ("dense_values" if "k_dense_values" in name else "dense" if "k_dense" in name else
+               "slices" if "k_slices" in name else "tiles")
         if key not in out:
             out[key] = get(v, "dram__bytes_read.sum") + get(v, "dram__bytes_write.sum")
     return out
