@@ -558,7 +558,10 @@ int launch_values(Handle* h, const Acc* x, double* y, cudaStream_t s, bool last)
   h->pdl_next = last && h->pdl && h->n_waves && !h->profiling && !h->signal_blocks && !h->d_trace;
   if (h->pdl_next) DG_CUDA(cudaMemsetAsync(h->d_counters, 0, Handle::kMaxWaves * sizeof(uint32_t), s));
   const int grid = h->pdl_next ? h->sm_count * 4 : grid_for(h->n_value_rows * 32ull, 256, 8);
-  k_dense_values<Acc, 2><<<grid, 256, 0, s>>>(
+  static const int cfg = [] { const char* c = std::getenv("DG_VALUES_CFG"); return c ? std::atoi(c) : 0; }();
+  auto kern = cfg == 1 ? k_dense_values<Acc, 4> : cfg == 2 ? k_dense_values<Acc, 8> :
+              cfg == 3 ? k_dense_values<Acc, 0> : k_dense_values<Acc, 2>;
+  kern<<<grid, 256, 0, s>>>(
       reinterpret_cast<const uint4*>(h->d_vstream), static_cast<const DenseRow*>(h->d_vrows),
       static_cast<uint32_t>(h->n_value_rows), x, static_cast<uint32_t>(h->cols), h->d_value_counter, y, h->gt);
   h->post(s, "dense_values", h->n_value_rows, h->value_nnz);

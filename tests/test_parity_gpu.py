@@ -634,3 +634,68 @@ def test_batch_width_both_paths_desk(port, golden, desk, monkeypatch, short):
     m = _wide_row_matrix(port, rows=2000, split=False)
     x = port.seeded_vector(m.cols, 42)
     assert np.array_equal(bits(dg.spmv_rowchunk(to_dg(m), x)), bits(port.spmv_rowchunk(m, x, 32, 2)))
+
+
+@pytest.mark.parametrize("min_len", ["4096", "64"])
+@pytest.mark.parametrize("iw", [U16, U32])
+def test_contiguous_rows_values_only_bit_exact(port, monkeypatch, min_len, iw):
+    """Contiguous rows (columns lo .. lo + len - 1) of at least DG_DENSE_MIN_LEN go to
+    k_dense_values as binary16 values alone (the column is lo + position).  Rows start at column
+    0 and end at the last column, have lengths around the 256-position batch edges, and end right
+    before 'poison' columns that no row touches, where x is +Inf or NaN: a padding position that
+    read x past the row's end (instead of the staged +0.0) would turn the row into NaN.  Exact
+    family bit-identical to the reference (device and host d, repeated doses); fp32 family within
+    tolerance; the device copy decodes back to the same arrays."""
+    import torch
+    monkeypatch.setenv("DG_DENSE_MIN_LEN", min_len)
+    rng = np.random.default_rng(21)
+    cols = 20_000
+    poison = np.array([5000, 10_000, 15_000])
+    rows_cols = []
+    ok = np.setdiff1d(np.arange(cols), poison)
+    for p in poison:  # contiguous rows ending right before / starting right after a poison column
+        for n in (64, 255, 256, 257, 4096, 4097, 4999):
+            rows_cols.append(np.arange(p - n, p))
+            rows_cols.append(np.arange(p + 1, min(cols, p + 1 + n)))
+    rows_cols += [np.arange(0, 4100), np.arange(cols - 4600, cols), np.arange(0, 4999)]
+    for _ in range(150):  # contiguous rows of random lengths inside a poison-free span
+        n = int(rng.integers(32, 4999))
+        seg = int(rng.integers(0, 4))
+        lo0, hi0 = (0, 5000) if seg == 0 else (poison[seg - 1] + 1, poison[seg] if seg < 3 else cols)
+        if hi0 - lo0 > n:
+            lo = int(rng.integers(lo0, hi0 - n))
+            rows_cols.append(np.arange(lo, lo + n))
+    for _ in range(150):  # sparse rows avoiding the poison columns
+        n = int(rng.integers(1, 3000))
+        rows_cols.append(np.sort(rng.choice(ok, n, replace=False)))
+    rows_cols += [np.array([], dtype=np.int64)] * 40
+    rng.shuffle(rows_cols)
+    lens = np.array([len(c) for c in rows_cols])
+    rp = np.zeros(len(rows_cols) + 1, dtype=np.uint64)
+    np.cumsum(lens, out=rp[1:])
+    col = np.concatenate(rows_cols).astype(np.uint32)
+    m = Csr(len(rows_cols), cols, HALF, iw, rp, col, _edge_values(rng, len(col)))
+    x = rng.standard_normal(cols) * np.exp(rng.uniform(-20, 20, cols))
+    x[poison] = [np.inf, np.nan, -np.inf]
+    want = bits(port.spmv_rowchunk(m, x, 32, 2))
+    assert not np.isnan(want.view(np.float64)).any()
+    with dg.DoseEngine.from_csr(to_dg(m)) as e:
+        yd = torch.empty(m.rows, dtype=torch.float64, device="cuda")
+        for _ in range(2):
+            assert np.array_equal(bits(e.dose(x)), want)
+            e.dose_device(torch.from_numpy(x).cuda().data_ptr(), m.cols, yd.data_ptr())
+            assert np.array_equal(yd.cpu().numpy().view(np.uint64), want)
+        back = e.copy_rows(0, m.rows)
+        assert np.array_equal(back.row_ptr, m.row_ptr)
+        assert np.array_equal(back.col_indices, m.col)
+        assert np.array_equal(back.values, m.values)
+    # fp32 family on the dose data's value ranges (positive halves, x in [0, 1)) with the same
+    # poison columns: tolerance against the oracle
+    vpos = (rng.random(len(col)) * (1 - 2.0 ** -14) + 2.0 ** -14).astype(np.float16).view(np.uint16)
+    mp = Csr(m.rows, cols, HALF, iw, rp, col, vpos)
+    xp = rng.random(cols)
+    xp[poison] = np.inf
+    ref = port.spmv_rowchunk(mp, xp, 32, 2)
+    with dg.DoseEngine.from_csr(to_dg(mp), accumulation=dg.ACCUM_FP32) as e:
+        got = e.dose(xp)
+        assert np.max(np.abs(got - ref)) <= FP32_TOL * np.max(np.abs(ref))
