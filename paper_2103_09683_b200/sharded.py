@@ -6,9 +6,8 @@ src/spmv.cpp:53-67), so the matrix is cut into nnz-balanced contiguous row block
 is an all-gather of the dose slices -- used only when the full d must be resident on a device.
 Output bits are identical for any number of GPUs (the row plan is per-row).
 
-The d slices are unequal, so the all-gather pads every slice to the largest shard and compacts
-(NCCL has no allgatherv); ``gather_dose`` does that on whatever backend the process group uses
-(NCCL on B200s, gloo in the CPU tests).
+The d slices are unequal; ``gather_dose`` is an allgatherv made of one broadcast per shard into
+place (grouped into one NCCL collective on B200s; plain broadcasts on gloo in the CPU tests).
 """
 from __future__ import annotations
 
@@ -40,20 +39,34 @@ def _torch_stream(device: int) -> int:
     return torch.cuda.current_stream(device).cuda_stream or CUDA_STREAM_LEGACY
 
 
-def gather_dose(y_local, bounds: Sequence[int], group=None):
-    """All-gather unequal d slices into the full d on every rank (torch tensors, same device as
-    y_local).  Pads to the largest slice, gathers, compacts."""
+def gather_dose(y_local, bounds: Sequence[int], group=None, out=None):
+    """Allgatherv of the unequal d slices into the full d on every rank (torch tensors on
+    y_local's device): this rank's slice is copied into place, then one broadcast per shard g
+    (root g) writes rows [bounds[g], bounds[g+1]) of every rank's full d directly -- no padding,
+    no compaction.  On NCCL the broadcasts are issued as one group
+    (ncclGroupStart / ncclGroupEnd through torch's coalescing manager), so they run as a single
+    fused collective."""
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
-    sizes = [int(bounds[g + 1] - bounds[g]) for g in range(world)]
-    cap = max(sizes) if sizes else 0
-    padded = torch.zeros(cap, dtype=y_local.dtype, device=y_local.device)
-    padded[: y_local.numel()] = y_local
-    parts = [torch.empty(cap, dtype=y_local.dtype, device=y_local.device) for _ in range(world)]
-    dist.all_gather(parts, padded, group=group)
-    return torch.cat([parts[g][: sizes[g]] for g in range(world)])
+    me = dist.get_rank(group)
+    n = int(bounds[world])
+    full = out if out is not None else torch.empty(n, dtype=y_local.dtype, device=y_local.device)
+    full[int(bounds[me]):int(bounds[me + 1])].copy_(y_local)
+    parts = [(g, full[int(bounds[g]):int(bounds[g + 1])]) for g in range(world)
+             if bounds[g + 1] > bounds[g]]
+    src = (lambda g: dist.get_global_rank(group, g)) if group is not None else (lambda g: g)
+    cm = getattr(dist, "_coalescing_manager", None)
+    if dist.get_backend(group) == "nccl" and cm is not None:
+        with cm(group=group, device=y_local.device, async_ops=True) as grouped:
+            for g, part in parts:
+                dist.broadcast(part, src=src(g), group=group)
+        grouped.wait()
+    else:
+        for g, part in parts:
+            dist.broadcast(part, src=src(g), group=group)
+    return full
 
 
 class ShardedDose:
