@@ -56,7 +56,7 @@ struct Handle {
   bool slots_encoded = false;      // the stream's slot-mode positions hold slots (else columns)
   // slice stream (spmv_slices.cuh, slices.cu): binary16 matrices under lane_width 32
   static constexpr int kSliceWarps = 32;       // warps per CTA of k_slices
-  static constexpr int kSliceWarpsCarry = 20;  // ... with carried partials (split rows)
+  static constexpr int kSliceWarpsCarry = 28;  // ... with carried partials (r02 C4: 20 / 24 / 26 / 28 / 32 warps 4.11 / 3.79 / 3.79 / 3.66 / 4.34 ms; 28 = 72 registers)
   bool slices_wanted = false;      // plan for the slice stream (DG_SLICES=0: row-ordered k_tiles)
   bool slices = false;             // the plan has one; d_slices holds it
   static constexpr int kRunsPerWarp = 2;     // runs per tile = kRunsPerWarp x warps (pulled dynamically)
@@ -123,7 +123,7 @@ struct Handle {
 
   // output row blocks (plan.cu): the d download of block k overlaps the kernel's later blocks
   static constexpr uint32_t kMaxBlocks = 64;     // DG_BLOCKS range
-  static constexpr uint32_t kDefaultBlocks = 32;  // C2: device step unchanged vs 8, e2e 2.87 -> 2.81
+  static constexpr uint32_t kDefaultBlocks = 16;  // r02 C2 e2e: 16 blocks 2.12-2.14 ms, 32: 2.19-2.27, 64: 2.44-2.47
   uint32_t n_blocks = 1;
   uint64_t blk_row0[kMaxBlocks + 1] = {};
   uint32_t blk_tiles[kMaxBlocks] = {};
