@@ -20,7 +20,7 @@ namespace dg {
 // dynamically, so the runs still left when a warp frees up are the shortest (online LPT): the
 // tile's window is released when the slowest warp is done, and a static run per warp left ~25% of
 // warp time waiting on a window on C2's 1/8 shard (DG_TRACE).  Each run is padded to whole
-// 4-chunk blocks (512 B).
+// 8-chunk batches (two 512-byte blocks), so the kernel's loads need no guards.
 int plan_slices(Handle* h, const std::vector<Tile>& tiles, std::vector<Segment>& segs) {
   const int WARPS = h->n_carry_slots ? Handle::kSliceWarpsCarry : Handle::kSliceWarps;
   int RUNS = WARPS * Handle::kRunsPerWarp;
@@ -381,7 +381,7 @@ int build_slices(Handle* h) {
       const uint32_t nch = static_cast<uint32_t>((rp[r + 1] - rp[r] + 31) / 32);
       R[k] = {static_cast<uint32_t>(c), static_cast<uint32_t>(k)};
       S[k] = {r, 0, nch, static_cast<uint32_t>(kSegFirst | kSegLast)};
-      c += (nch + kSliceBlock - 1) / kSliceBlock * kSliceBlock;
+      c += (nch + kSlicePad - 1) / kSlicePad * kSlicePad;
       if (c > 0xFFFFFFFFull) return DG_ERR_UNSUPPORTED_FEATURE;
       tile_row[r] = 1;  // not in the rest stream
     }
@@ -500,7 +500,10 @@ template <typename Acc>
 int launch_slices(Handle* h, const Acc* x, double* y, cudaStream_t s) {
   const size_t smem = 2ull * h->window_cols * sizeof(Acc);
   const bool carry = h->n_carry_slots != 0;
-  constexpr int kP = std::is_same_v<Acc, float> ? 4 : 2;
+#ifndef DG_SLICE_P_EXACT
+#define DG_SLICE_P_EXACT 2
+#endif
+  constexpr int kP = std::is_same_v<Acc, float> ? 4 : DG_SLICE_P_EXACT;
   auto kern = carry ? k_slices<Acc, Handle::kSliceWarpsCarry, kP, true>
                     : k_slices<Acc, Handle::kSliceWarps, kP, false>;
   const int warps = carry ? Handle::kSliceWarpsCarry : Handle::kSliceWarps;

@@ -44,10 +44,10 @@ struct SliceSeg {
 
 constexpr int kSliceU = 8;      // chunks per batch (two 512-byte blocks)
 #ifndef DG_SLICE_PAD
-#define DG_SLICE_PAD 4
+#define DG_SLICE_PAD 8
 #endif
 constexpr int kSliceBlock = 4;  // chunks per block
-constexpr int kSlicePad = DG_SLICE_PAD;  // runs are padded to whole multiples of this many chunks
+constexpr int kSlicePad = DG_SLICE_PAD;  // runs are padded to whole multiples of this many chunks (whole batches)
 
 __device__ __forceinline__ uint4 ld_stream16(const uint4* p) {
   uint4 v;
@@ -57,10 +57,12 @@ __device__ __forceinline__ uint4 ld_stream16(const uint4* p) {
   return v;
 }
 
-// One warp's run: nblk 4-chunk blocks starting at chunk c0 (a multiple of 4), consumed in batches
-// of two blocks; an odd last block is paired with neutral words (`neutral`: the zero slot, value
-// +0).  Software pipeline: batch b + 1 is in flight in registers while batch b is gathered and
-// accumulated; lanes 0..7 prefetch the 8 lines of batch b + 1 + P into L2.
+// One warp's run: nblk 4-chunk blocks starting at chunk c0 (a multiple of 8), consumed in batches
+// of two blocks (runs are padded to whole batches with neutral words: the zero slot, value +0).
+// Software pipeline: batch b + 1 is in flight in registers while batch b is gathered and
+// accumulated; lanes 0..7 prefetch the 8 lines of batch b + 1 + P into L2.  r02: whole-batch
+// padding (no guarded second load, no neutral fill), a pointer-stepped prefetch stream and
+// mask-predicated segment ends (products once) trimmed the per-batch instructions.
 // x sources of a run: the tile's shared-memory window (indexed by slot) or global x (dense rows:
 // their 32 lanes read consecutive columns, through L1 / L2)
 template <typename Acc>
@@ -82,8 +84,10 @@ __device__ __forceinline__ void run_slice(const uint4* __restrict__ blocks, uint
                                           const GatherTargets& gt, uint32_t lane) {
   using Ops = AccOps<Acc>;
   if (nblk == 0) return;
-  const uint32_t nb = (nblk + 1) / 2;  // batches
-  const uint4 pad = make_uint4(neutral, neutral, neutral, neutral);
+  // runs are padded to whole batches (kSlicePad = 8 chunks = 2 blocks): both blocks of every
+  // batch exist, so the loads need no guard and no neutral fill
+  static_assert(kSlicePad % (2 * kSliceBlock) == 0, "runs must hold whole batches");
+  const uint32_t nb = nblk / 2;  // batches
   // current segment and the next one's descriptor (loaded one segment ahead)
   uint32_t si = s0;
   SliceSeg cur = sseg[si];
@@ -91,14 +95,14 @@ __device__ __forceinline__ void run_slice(const uint4* __restrict__ blocks, uint
   uint32_t left = cur.nch;
   Acc acc = CARRY ? carry.in(cur.slot, cur.flags, lane) : Acc(0);
   const uint4* p = blocks + static_cast<uint64_t>(c0 / 4) * 32 + lane;  // block c0/4, lane's 16 B
-  uint4 a0 = ld_stream16(p), a1 = nblk > 1 ? ld_stream16(p + 32) : pad, b0, b1;
-  // line l (< 8) of batch k: block 2k + (l >= 4)
-  auto pf_ok = [&](uint32_t k) { return 2 * k + (lane >= 4 ? 1u : 0u) < nblk; };
+  uint4 a0 = ld_stream16(p), a1 = ld_stream16(p + 32), b0, b1;
+  // L2 prefetch stream: lanes 0..7 each own one 128-byte line of a batch (1 KB), P batches ahead
+  const char* pf = reinterpret_cast<const char*>(p - lane) + 128 * lane;
   if constexpr (P > 0) {
 #pragma unroll
     for (int k = 1; k <= P; ++k)
-      if (lane < 8 && pf_ok(k))
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(p - lane + 64 * k) + 128 * lane));
+      if (lane < 8 && static_cast<uint32_t>(k) < nb) asm volatile("prefetch.global.L2 [%0];" ::"l"(pf + 1024 * k));
+    pf += 1024 * (P + 1);
   }
   auto finish = [&]() {  // the current segment ends with the chunk just added
     if (!CARRY || (cur.flags & kSegLast)) {
@@ -134,53 +138,46 @@ __device__ __forceinline__ void run_slice(const uint4* __restrict__ blocks, uint
       left -= kSliceU;
       return;
     }
-#ifndef DG_SLICE_ONE_FINISH
-#define DG_SLICE_ONE_FINISH 1
-#endif
-    if (DG_SLICE_ONE_FINISH) {
-      // segment ends inside the batch: words [k, e) of the current segment are added in position
-      // order (predicated), then one finish() -- a single inlined copy of the row epilogue
-      // instead of one per word (code size: the kernel's hot loop stays in the instruction cache)
-      uint32_t k = 0;
-      do {
-        const uint32_t e = left >= kSliceU - k ? static_cast<uint32_t>(kSliceU) : k + left;
+    // segment end(s) inside the batch: the products once, then each segment's chunks [k, e)
+    // added in position order under a warp-uniform bit mask, one finish() per segment end
+    Acc pr[kSliceU];
 #pragma unroll
-        for (int j = 0; j < kSliceU; ++j)
-          if (j >= static_cast<int>(k) && j < static_cast<int>(e))
-            acc = Ops::add(acc, Ops::prod(static_cast<uint16_t>(r[j] & 0xFFFFu), xv[j]));
-        left -= e - k;
-        k = e;
-        if (left == 0) finish();
-      } while (k < static_cast<uint32_t>(kSliceU));
-      return;
-    }
+    for (int j = 0; j < kSliceU; ++j) pr[j] = Ops::prod(static_cast<uint16_t>(r[j] & 0xFFFFu), xv[j]);
+    uint32_t k = 0;
+    do {
+      const uint32_t e = left >= kSliceU - k ? static_cast<uint32_t>(kSliceU) : k + left;
+      const uint32_t m = (0xFFu >> (kSliceU - (e - k))) << k;  // chunks k .. e-1
 #pragma unroll
-    for (int k = 0; k < kSliceU; ++k) {
-      acc = Ops::add(acc, Ops::prod(static_cast<uint16_t>(r[k] & 0xFFFFu), xv[k]));
-      if (--left == 0) finish();
-    }
+      for (int j = 0; j < kSliceU; ++j)
+        if (m & (1u << j)) acc = Ops::add(acc, pr[j]);
+      left -= e - k;
+      k = e;
+      if (left == 0) finish();
+    } while (k < static_cast<uint32_t>(kSliceU));
   };
   uint32_t bi = 0;
   for (;;) {
     // step A: consume a, load b
     if (bi + 1 < nb) {
       b0 = ld_stream16(p + 64);
-      b1 = 2 * bi + 3 < nblk ? ld_stream16(p + 96) : pad;
+      b1 = ld_stream16(p + 96);
     }
-    if constexpr (P > 0)
-      if (lane < 8 && pf_ok(bi + 1 + P))
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(p - lane + 64 * (1 + P)) + 128 * lane));
+    if constexpr (P > 0) {
+      if (lane < 8 && bi + 1 + P < nb) asm volatile("prefetch.global.L2 [%0];" ::"l"(pf));
+      pf += 1024;
+    }
     consume(a0, a1);
     if (++bi == nb) break;
     p += 64;
     // step B: consume b, load a
     if (bi + 1 < nb) {
       a0 = ld_stream16(p + 64);
-      a1 = 2 * bi + 3 < nblk ? ld_stream16(p + 96) : pad;
+      a1 = ld_stream16(p + 96);
     }
-    if constexpr (P > 0)
-      if (lane < 8 && pf_ok(bi + 1 + P))
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(p - lane + 64 * (1 + P)) + 128 * lane));
+    if constexpr (P > 0) {
+      if (lane < 8 && bi + 1 + P < nb) asm volatile("prefetch.global.L2 [%0];" ::"l"(pf));
+      pf += 1024;
+    }
     consume(b0, b1);
     if (++bi == nb) break;
     p += 64;
@@ -349,8 +346,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 
 // ---- dense rows over the slice layout ---------------------------------------------------------
 // The dense rows k_dense owns (>= 3/4 of their span, the longest rows) as runs of one segment
-// each, longest first, in the same lane-major 4-chunk blocks: each row starts on a 512-byte block
-// (its lane grid = the row's, lane0 0) and is padded to whole blocks with neutral words whose
+// each, longest first, in the same lane-major 4-chunk blocks: each row starts on a 1-KB batch
+// (its lane grid = the row's, lane0 0) and is padded to whole batches with neutral words whose
 // column is `cols` (x[cols] is a staged +0.0).  Warps of persistent 8-warp CTAs pull rows
 // longest first and stream them with the tile kernel's run pipeline (two LDG.128 per lane per
 // 8-chunk batch, L2 prefetch P batches ahead); x comes from global memory through L1.
