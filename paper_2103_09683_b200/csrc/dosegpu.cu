@@ -743,7 +743,10 @@ int dg_dose(dg_handle* hh, const double* x, uint64_t x_len, double* y, uint32_t 
   const char* no_ovl = std::getenv("DG_NO_OVERLAP");
   // (single-wave plans only: with split rows every block's last tiles are in the last waves, so
   //  the blocks complete at the very end -- C4 end to end 7.24 ms overlapped vs 7.16 plain; r02
-  //  with the slice kernel: 4.82 vs 4.59 ms, and 4.78-4.83 with wave lags 1 / 2 / 4)
+  //  with the slice kernel: 4.82 vs 4.59 ms, and 4.78-4.83 with wave lags 1 / 2 / 4).
+  // (measured, rejected: with pinned host d, running the contiguous rows LAST -- after the block
+  //  downloads, storing their rows into the pinned d zero-copy -- C2 end to end 2.10 vs 2.10 ms:
+  //  the 64 MB download runs at ~45 GB/s beside the kernels either way, 1.42 ms)
   const bool overlap = !y_dev && h->rows && h->use_tiles && h->n_waves == 1 &&
                        h->n_blocks > 1 && dg::wait_value_fn() && !(no_ovl && *no_ovl == '1');
   h->signal_blocks = overlap;

@@ -648,6 +648,7 @@ def test_contiguous_rows_values_only_bit_exact(port, monkeypatch, min_len, iw):
     tolerance; the device copy decodes back to the same arrays."""
     import torch
     monkeypatch.setenv("DG_DENSE_MIN_LEN", min_len)
+    monkeypatch.setenv("DG_BLOCKS", "4")  # the overlapped host download
     rng = np.random.default_rng(21)
     cols = 20_000
     poison = np.array([5000, 10_000, 15_000])
@@ -681,10 +682,16 @@ def test_contiguous_rows_values_only_bit_exact(port, monkeypatch, min_len, iw):
     assert not np.isnan(want.view(np.float64)).any()
     with dg.DoseEngine.from_csr(to_dg(m)) as e:
         yd = torch.empty(m.rows, dtype=torch.float64, device="cuda")
+        xh = torch.from_numpy(x).pin_memory()
+        yh = torch.full((m.rows,), 7.0, dtype=torch.float64).pin_memory()
         for _ in range(2):
-            assert np.array_equal(bits(e.dose(x)), want)
+            assert np.array_equal(bits(e.dose(x)), want)  # pageable host d
             e.dose_device(torch.from_numpy(x).cuda().data_ptr(), m.cols, yd.data_ptr())
             assert np.array_equal(yd.cpu().numpy().view(np.uint64), want)
+            # pinned host d: row blocks downloaded while the tile kernel runs
+            e.dose_host_ptrs(xh.data_ptr(), m.cols, yh.data_ptr())
+            assert np.array_equal(yh.numpy().view(np.uint64), want)
+            yh.fill_(7.0)
         back = e.copy_rows(0, m.rows)
         assert np.array_equal(back.row_ptr, m.row_ptr)
         assert np.array_equal(back.col_indices, m.col)
