@@ -479,13 +479,20 @@ def run_ours(args):
         return
     peak, peak_kind = measured_hbm_peak()
     achieved = dom["bytes"] / (dom["ms"] * 1e-3) / 1e9
-    traffic = None
+    traffic = traffic_step = None
     tf = os.path.join(ROOT, "profiles", "dram_bytes_per_launch.json")
     if os.path.exists(tf) and world == 1 and not args.rows:  # profiled: the full 1-GPU workload
         try:
             tj = json.load(open(tf))
-            traffic = tj.get(f"{args.config}:{args.accum}:{dom_name}",
-                             tj.get(f"{args.config}:{args.accum}:{dom_name.split('[')[0]}"))
+
+            def tget(name):
+                return tj.get(f"{args.config}:{args.accum}:{name}",
+                              tj.get(f"{args.config}:{args.accum}:{name.split('[')[0]}"))
+            traffic = tget(dom_name)
+            # DRAM bytes of the whole dose (every kernel with an ncu figure): with the value
+            # stream (implied column words) it is below the reference-model bytes
+            tk = [tget(k) for k in per]
+            traffic_step = int(sum(tk)) if tk and all(v is not None for v in tk) else None
         except Exception:
             traffic = None
     info = engines[0].info
@@ -516,7 +523,8 @@ def run_ours(args):
         "frac_of_measured_hbm": total_bytes / (ms_step * 1e-3) / 1e9 / peak / world,
         "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "bytes_per_launch": dom["bytes"] / len(engines),
+                     "traffic": traffic, "traffic_step_ncu": traffic_step,
+                     "bytes_per_launch": dom["bytes"] / len(engines),
                      "ms_per_launch": dom["ms"] / len(engines),
                      "share_of_step": dom["ms"] / (ms / args.steps if world == 1 else ms_step),
                      "kernels": {k: {"ms": round(v["ms"], 4), "bytes": int(v["bytes"])}

@@ -454,6 +454,11 @@ int build_slices(Handle* h) {
   h->d_row_ptr_orig = h->d_row_ptr;
   h->d_row_ptr = d_rest_rp;
   h->rest_nnz = rest_nnz;
+  // resident matrix bytes now: both row pointers, the slice / dense-slice / value streams and the
+  // rest stream (dg_get_info.device_bytes)
+  h->matrix_bytes = 2 * (h->rows + 1) * 8 + (h->slice_chunks + h->dense_chunks) * 32 * 4 +
+                    h->value_blocks * 32 * kValueChunks * 2 +
+                    rest_nnz * (h->packed ? 4 : h->index_bytes + 2);
   return DG_OK;
 }
 
