@@ -7,7 +7,7 @@ is an all-gather of the dose slices -- used only when the full d must be residen
 Output bits are identical for any number of GPUs (the row plan is per-row).
 
 The d slices are unequal; ``gather_dose`` is an allgatherv made of one broadcast per shard into
-place (grouped into one NCCL collective on B200s; plain broadcasts on gloo in the CPU tests).
+place (NCCL on B200s, gloo in the CPU tests).
 """
 from __future__ import annotations
 
@@ -43,9 +43,9 @@ def gather_dose(y_local, bounds: Sequence[int], group=None, out=None):
     """Allgatherv of the unequal d slices into the full d on every rank (torch tensors on
     y_local's device): this rank's slice is copied into place, then one broadcast per shard g
     (root g) writes rows [bounds[g], bounds[g+1]) of every rank's full d directly -- no padding,
-    no compaction.  On NCCL the broadcasts are issued as one group
-    (ncclGroupStart / ncclGroupEnd through torch's coalescing manager), so they run as a single
-    fused collective."""
+    no compaction.  The broadcasts are issued one after another (async, then
+    waited): plain collectives every backend supports (the in-process C-ABI path, dg_multi,
+    groups them into one NCCL call)."""
     import torch
     import torch.distributed as dist
 
@@ -54,18 +54,14 @@ def gather_dose(y_local, bounds: Sequence[int], group=None, out=None):
     n = int(bounds[world])
     full = out if out is not None else torch.empty(n, dtype=y_local.dtype, device=y_local.device)
     full[int(bounds[me]):int(bounds[me + 1])].copy_(y_local)
-    parts = [(g, full[int(bounds[g]):int(bounds[g + 1])]) for g in range(world)
-             if bounds[g + 1] > bounds[g]]
-    src = (lambda g: dist.get_global_rank(group, g)) if group is not None else (lambda g: g)
-    cm = getattr(dist, "_coalescing_manager", None)
-    if dist.get_backend(group) == "nccl" and cm is not None:
-        with cm(group=group, device=y_local.device, async_ops=True) as grouped:
-            for g, part in parts:
-                dist.broadcast(part, src=src(g), group=group)
-        grouped.wait()
-    else:
-        for g, part in parts:
-            dist.broadcast(part, src=src(g), group=group)
+    works = []
+    for g in range(world):
+        if bounds[g + 1] > bounds[g]:
+            src = dist.get_global_rank(group, g) if group is not None else g
+            works.append(dist.broadcast(full[int(bounds[g]):int(bounds[g + 1])], src=src,
+                                        group=group, async_op=True))
+    for w in works:
+        w.wait()
     return full
 
 
