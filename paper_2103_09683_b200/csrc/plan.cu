@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
 #include <cstdlib>
 #include <numeric>
 #include <vector>
@@ -227,8 +228,21 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
   h->n_split_rows = wide.size();
   h->n_dense_rows = dense_rows.size();
   if (!dense_rows.empty()) {  // longest first: the pool ends with the shortest rows
-    std::stable_sort(dense_rows.begin(), dense_rows.end(),
-                     [&](uint32_t a, uint32_t b) { return lens[a] > lens[b]; });
+    // Pull order: longest first by power-of-two length class (the kernel's tail is the last rows
+    // pulled), by first column within a class -- rows running at the same time then overlap in
+    // x, which the dense kernels read through L1 (an SM's L1 holds ~80% of C2's 320-KB x; rows
+    // spread over all of x miss ~half the time, and a miss costs L1 data-pipe fills on top of the
+    // hits -- the kernel's roof; C2 k_dense_values 0.525 -> 0.472 ms).  The fp32 family's x
+    // (160 KB) fits L1 whole: strictly longest first there (the class order's longer tail cost
+    // it ~2%).  DG_DENSE_ORDER=len / cls overrides.
+    const char* dord = std::getenv("DG_DENSE_ORDER");
+    const bool by_len = dord ? std::strcmp(dord, "len") == 0 : h->accumulation == DG_ACCUM_FP32;
+    auto cls = [&](uint32_t r) { return 63 - __builtin_clzll(lens[r] | 1); };
+    std::stable_sort(dense_rows.begin(), dense_rows.end(), [&](uint32_t a, uint32_t b) {
+      if (by_len) return lens[a] > lens[b];
+      const int ca = cls(a), cb = cls(b);
+      return ca != cb ? ca > cb : ext[a].x < ext[b].x;
+    });
     h->dense_contig.resize(dense_rows.size());
     for (size_t i = 0; i < dense_rows.size(); ++i) h->dense_contig[i] = contiguous(dense_rows[i]);
     DG_CUDA(cudaMalloc(&h->d_dense_rows, dense_rows.size() * sizeof(uint32_t)));

@@ -139,6 +139,10 @@ __global__ void k_fill_words(uint32_t* s, const Row* rows, uint32_t n_rows) {
 
 int main(int argc, char** argv) {
   const uint32_t cols = 40000;
+  // argv[1]: max row length (default 40000); argv[2]: columns the rows' starts are spread over
+  // (default: all) -- a narrow spread is a small x footprint per SM (L1 locality experiment)
+  const uint32_t max_len = argc > 1 ? (uint32_t)atoi(argv[1]) : 40000;
+  const uint32_t lo_span = argc > 2 ? (uint32_t)atoi(argv[2]) : 0;
   // C2's dense rows: ~1.34e9 nonzeros in rows of 4,096 .. 40,000 (longest first, as k_dense pulls)
   std::vector<Row> rows;
   std::vector<uint32_t> lens;
@@ -146,7 +150,7 @@ int main(int argc, char** argv) {
   srand(1);
   while (nnz < 1340000000ull) {
     const double u = rand() / (double)RAND_MAX;
-    uint32_t len = (uint32_t)(4096 * __builtin_pow(40000.0 / 4096, u * u));
+    uint32_t len = (uint32_t)(4096 * __builtin_pow(max_len / 4096.0, u * u));
     lens.push_back(len);
     nnz += len;
   }
@@ -154,7 +158,8 @@ int main(int argc, char** argv) {
   uint64_t off_v = 0, off_w = 0;
   std::vector<Row> rv, rw;
   for (uint32_t len : lens) {
-    const uint32_t lo = rand() % (cols - len + 1);
+    const uint32_t room = lo_span ? std::min(lo_span, cols - len + 1) : cols - len + 1;
+    const uint32_t lo = rand() % room;
     const uint32_t nch = (len + 31) / 32;
     rv.push_back({off_v, lo, len});
     rw.push_back({off_w, lo, len});
@@ -202,7 +207,7 @@ int main(int argc, char** argv) {
            nnz / best / 1e6, bytes / best / 1e6, nnz * 4.0 / best / 1e6, cudaGetErrorString(cudaGetLastError()));
   };
   const uint32_t n = (uint32_t)lens.size();
-  for (int g : {4, 8}) {
+  for (int g : {4}) {
     char nm[64];
     snprintf(nm, sizeof nm, "words (4 B) P4 grid %dxSM", g);
     time(nm, [&] { k_words<4><<<g * sms, 256>>>(sw, drw, n, x, cnt, y); }, off_w * 16.0);
