@@ -237,7 +237,13 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     // it ~2%).  DG_DENSE_ORDER=len / cls overrides.
     const char* dord = std::getenv("DG_DENSE_ORDER");
     const bool by_len = dord ? std::strcmp(dord, "len") == 0 : h->accumulation == DG_ACCUM_FP32;
-    auto cls = [&](uint32_t r) { return 63 - __builtin_clzll(lens[r] | 1); };
+    static const int cls_shift = [] { const char* c = std::getenv("DG_DENSE_CLASS"); return c ? std::atoi(c) : 0; }();
+    auto cls = [&](uint32_t r) {  // length class: octave (DG_DENSE_CLASS=1: half octave, 2: two octaves)
+      const int o = 63 - __builtin_clzll(lens[r] | 1);
+      if (cls_shift == 1) return 2 * o + static_cast<int>((lens[r] >> (o - 1)) & 1);
+      if (cls_shift == 2) return o / 2;
+      return o;
+    };
     std::stable_sort(dense_rows.begin(), dense_rows.end(), [&](uint32_t a, uint32_t b) {
       if (by_len) return lens[a] > lens[b];
       const int ca = cls(a), cb = cls(b);
