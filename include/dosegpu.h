@@ -197,6 +197,8 @@ typedef struct {
   uint64_t nonempty_rows;
   uint32_t n_kernels;                /* kernels launched per dg_dose (device-resident x/y) */
   int32_t device;
+  uint64_t read_ns;                  /* dg_create_from_ddm: wall time reading the file's row_ptr,
+                                        column and value sections into device memory (0 else) */
 } dg_info;
 int dg_get_info(const dg_handle* h, dg_info* info);
 

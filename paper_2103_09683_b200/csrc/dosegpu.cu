@@ -799,6 +799,7 @@ int dg_get_info(const dg_handle* hh, dg_info* info) {
   info->nonempty_rows = h->nonempty_rows;
   info->n_kernels = h->n_kernels ? h->n_kernels : h->expected_kernels();
   info->device = h->device;
+  info->read_ns = h->read_ns;
   return DG_OK;
 }
 

@@ -37,6 +37,7 @@ struct Handle {
   uint32_t* d_packed = nullptr;
   bool packed = false;
   uint64_t matrix_bytes = 0;
+  uint64_t read_ns = 0;  // dg_create_from_ddm: file sections -> device (dg_info.read_ns)
 
   // row plan: short-row bins ...
   uint32_t* d_bin[kNumBins] = {};

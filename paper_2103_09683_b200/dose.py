@@ -94,7 +94,8 @@ class _Info(C.Structure):
                 ("value_bytes", C.c_uint32), ("index_bytes", C.c_uint32),
                 ("lane_width", C.c_uint32), ("accumulation", C.c_uint32),
                 ("device_bytes", C.c_uint64), ("model_bytes", C.c_uint64),
-                ("nonempty_rows", C.c_uint64), ("n_kernels", C.c_uint32), ("device", C.c_int32)]
+                ("nonempty_rows", C.c_uint64), ("n_kernels", C.c_uint32), ("device", C.c_int32),
+                ("read_ns", C.c_uint64)]
 
 
 class _Timing(C.Structure):
