@@ -19,6 +19,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <new>
 #include <vector>
@@ -158,11 +159,28 @@ int to_beams(const dg_profile* p, uint32_t n, Beams* out, uint64_t* rows, uint64
   uint64_t off = 0;
   for (uint32_t k = 0; k < n; ++k) {
     const dg_profile& q = p[k];
-    // matgen.cpp:96-126 range checks (the +-10% expected-ratio check is the profile author's).
+    // ddm::validate_profile (matgen.cpp:96-126), same checks, order and Errc: ranges, then the
+    // expected-value consistency of the length distribution with the target ratio (+-10%)
     if (q.rows < 1 || q.cols < 1) return DG_ERR_INVALID_CONFIG;
-    if (!(q.empty_row_fraction >= 0.0 && q.empty_row_fraction <= 1.0)) return DG_ERR_INVALID_CONFIG;
+    auto fraction = [](double f) { return f >= 0.0 && f <= 1.0; };
+    if (!fraction(q.target_nnz_ratio)) return DG_ERR_INVALID_CONFIG;
+    if (!fraction(q.empty_row_fraction)) return DG_ERR_INVALID_CONFIG;
     if (!(q.row_length_log_sigma >= 0.0)) return DG_ERR_INVALID_CONFIG;
     if (q.locality_window < 1 || q.locality_window > q.cols) return DG_ERR_INVALID_CONFIG;
+    {
+      const double mean_len = std::min(
+          static_cast<double>(q.cols),
+          std::max(1.0, std::exp(q.row_length_log_mean +
+                                 0.5 * q.row_length_log_sigma * q.row_length_log_sigma)));
+      const double expected = (1.0 - q.empty_row_fraction) * mean_len / static_cast<double>(q.cols);
+      if (q.target_nnz_ratio == 0.0) {
+        if (q.empty_row_fraction != 1.0) return DG_ERR_INCONSISTENT_PROFILE;
+      } else {
+        if (q.empty_row_fraction == 1.0) return DG_ERR_INCONSISTENT_PROFILE;
+        if (std::fabs(expected - q.target_nnz_ratio) / q.target_nnz_ratio > 0.10)
+          return DG_ERR_INCONSISTENT_PROFILE;
+      }
+    }
     if (q.rows != p[0].rows) return DG_ERR_DIMENSION_MISMATCH;
     out->b[k] = {q.cols, q.locality_window, q.seed, off, q.empty_row_fraction,
                  q.row_length_log_mean, q.row_length_log_sigma};

@@ -180,3 +180,36 @@ def test_seeded_vector_equals_reference_at_config_sizes(ref, n, seed):
     a = dg.seeded_vector(n, seed)
     b = ref.seeded_vector(n, seed)
     assert np.array_equal(a.view(np.uint64), np.asarray(b, dtype=np.float64).view(np.uint64))
+
+
+@pytest.mark.parametrize("case", ["inconsistent", "ratio_above_1", "negative_sigma", "all_empty",
+                                  "zero_ratio_not_empty", "window_above_cols", "consistent"])
+def test_generator_profile_contract_matches_reference(case):
+    """dg_create_generated / dg_generated_row_lengths check a profile exactly as
+    ddm::validate_profile does (matgen.cpp:96-126): the same Errc in the same order -- ranges
+    (InvalidConfig), then the length distribution's expected nnz ratio within 10% of the target
+    (InconsistentProfile).  Profile errors come back before any device is touched (this runs on
+    the CPU); a consistent profile gets as far as the device (NoDevice here)."""
+    from oracle.oracle import Oracle, OracleError, Profile as OProfile, have_reference
+    base = [5000, 4096, 0.01, 0.70, 4.5741, 0.8278, 4096, 1]  # C1's profile, fewer rows
+    mod = {"inconsistent": (4, 5.5), "ratio_above_1": (2, 1.5), "negative_sigma": (5, -0.1),
+           "all_empty": (3, 1.0), "zero_ratio_not_empty": (2, 0.0), "window_above_cols": (6, 5000),
+           "consistent": None}[case]
+    if mod:
+        base[mod[0]] = mod[1]
+    want = 0
+    if have_reference():
+        try:
+            Oracle("reference").generate(OProfile(*base))
+        except OracleError as e:
+            want = e.code
+    else:  # the reference's Errc for each case (matgen.cpp:96-126)
+        want = {"inconsistent": 15, "all_empty": 15, "zero_ratio_not_empty": 15,
+                "consistent": 0}.get(case, 6)
+    with pytest.raises(dg.Error) as err:
+        dg.generated_row_lengths(dg.Profile(*base), 0, 10)
+    got = err.value.status
+    if want == 0:
+        assert got == 900  # NoDevice: the profile passed
+    else:
+        assert got == want, (case, got, want)
