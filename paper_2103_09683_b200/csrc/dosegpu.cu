@@ -17,30 +17,6 @@
 
 namespace dg {
 
-// ------------------------------------------------------------------------------------------
-// upload-time validation (ddm::validate, src/sparse.cpp:197-255): per row, columns strictly
-// increasing and < cols; every value finite.  Flags are OR-ed into *bad.
-template <class M>
-__global__ void k_validate(M mat, const uint64_t* __restrict__ rp, uint64_t rows, uint64_t cols,
-                           unsigned* __restrict__ bad) {
-  const uint64_t lane = threadIdx.x & 31;
-  const uint64_t warp = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
-  const uint64_t n_warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-  unsigned flag = 0;
-  for (uint64_t r = warp; r < rows; r += n_warps) {
-    const uint64_t s = rp[r], e = rp[r + 1];
-    for (uint64_t j = s + lane; j < e; j += 32) {
-      const auto el = mat.load(j);
-      const uint64_t c = M::c_of(el);
-      if (c >= cols) flag |= 1u;
-      if (j > s && c <= static_cast<uint64_t>(mat.col_at(j - 1))) flag |= 2u;
-      if (!isfinite(widen(M::v_of(el)))) flag |= 4u;
-    }
-  }
-  flag = __reduce_or_sync(kFull, flag);
-  if (lane == 0 && flag) atomicOr(bad, flag);
-}
-
 __global__ void k_narrow_u32_u16(const uint32_t* __restrict__ in, uint16_t* __restrict__ out,
                                  uint64_t n, uint64_t cols, unsigned* __restrict__ bad) {
   unsigned flag = 0;

@@ -26,6 +26,7 @@
 
 #include "common.cuh"
 #include "handle.cuh"
+#include "spmv_kernels.cuh"
 
 namespace dg {
 
@@ -288,7 +289,20 @@ int dg_create_generated(const dg_profile* p, uint32_t n_beams, uint32_t index_by
           static_cast<uint16_t*>(h->d_val), nullptr);
   }
   if ((st = cu(cudaGetLastError()))) return fail(st);
+  // ddm::validate's per-entry invariants on the generated matrix too (the reference validates
+  // every CsrMatrix it builds; one pass over the device copy)
+  if ((st = cu(cudaMemset(h->d_bad, 0, sizeof(unsigned))))) return fail(st);
+  st = dg::dispatch_mat(h, [&](const auto& mat) {
+    dg::k_validate<<<dg::grid_for(32 * n, 256), 256>>>(mat, h->d_row_ptr, n, h->cols, h->d_bad);
+    return cu(cudaGetLastError());
+  });
+  if (st) return fail(st);
   if ((st = cu(cudaDeviceSynchronize()))) return fail(st);
+  {
+    unsigned bad = 0;
+    if ((st = cu(cudaMemcpy(&bad, h->d_bad, sizeof(unsigned), cudaMemcpyDeviceToHost)))) return fail(st);
+    if (bad) return fail(DG_ERR_VALIDATION_FAILURE);
+  }
   h->matrix_bytes = (n + 1) * 8 + h->nnz * (2 + index_bytes);
   std::vector<uint64_t> lens(n);
   for (uint64_t r = 0; r < n; ++r) lens[r] = rp[r + 1] - rp[r];
