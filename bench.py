@@ -524,6 +524,10 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "traffic_step_ncu": traffic_step,
+                     "note": "achieved / value count the reference model's bytes ((vb+ib)*nnz + "
+                             "16*rows + 8*cols, perf_model.cpp:41-54); contiguous rows are "
+                             "streamed without their implied column words and U32 columns as "
+                             "16-bit window slots, so the DRAM bytes (traffic*) are fewer",
                      "bytes_per_launch": dom["bytes"] / len(engines),
                      "ms_per_launch": dom["ms"] / len(engines),
                      "share_of_step": dom["ms"] / (ms / args.steps if world == 1 else ms_step),
