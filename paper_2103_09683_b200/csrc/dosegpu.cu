@@ -292,6 +292,10 @@ int launch_tiles(Handle* h, const M& mat, const Acc* x, double* y, cudaStream_t 
                  const char* /*name*/) {
   // (measured, rejected: k_dense on a side stream beside a 24-warp tile kernel, one CTA of each
   //  per SM -- C2 3.89 ms vs 2.88 back to back; profiles/README.md)
+  // (measured, rejected: the contiguous rows AFTER the tile kernel as its programmatic dependent,
+  //  to fill the tile kernel's tail -- C2 1.97 vs 1.75 ms, C3 shard 0.29 vs 0.26: the value
+  //  kernel's CTAs then start on SMs still configured for the tile kernel's shared memory, and
+  //  it is L1-bound)
   DG_TRY(launch_dense(h, mat, x, y, s));
   if (!h->n_waves) return DG_OK;
   if (h->slices) return launch_slices<Acc>(h, x, y, s);
@@ -430,8 +434,10 @@ int finish_create(Handle* h, const std::vector<uint64_t>& lens) {
   // ~8 tiles per SM at least (small matrices), at most 768K nonzeros per tile (C2 sweep: 512K-768K
   // flat, 1M +0.6%, 1.5M +1%, with the rows wider than a window in k_dense; C4 / C5 flat)
   h->tile_nnz = std::max<uint64_t>(16 * 1024, std::min<uint64_t>(768 * 1024,
-                                                                  h->nnz / (8ull * h->sm_count)));
+                                                                  h->nnz / (h->min_tiles_per_sm * h->sm_count)));
   if (const char* tn = std::getenv("DG_TILE_NNZ")) h->tile_nnz = std::strtoull(tn, nullptr, 10);
+  if (const char* tp = std::getenv("DG_TILES_PER_SM"))
+    h->min_tiles_per_sm = std::max<uint64_t>(1, std::strtoull(tp, nullptr, 10));
   if (const char* tc = std::getenv("DG_TILE_CFG")) h->tile_cfg = std::atoi(tc);
   if (const char* tg = std::getenv("DG_TILE_GUIDE")) h->tile_guide = std::strtoull(tg, nullptr, 10);
   if (const char* tg = std::getenv("DG_TILE_GUIDE_MIN"))

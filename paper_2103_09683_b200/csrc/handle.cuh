@@ -73,6 +73,7 @@ struct Handle {
   uint64_t* d_row_ptr_orig = nullptr;
   uint64_t rest_nnz = 0;
   uint64_t tile_nnz = 768 * 1024;  // target nonzeros per tile (finish_create: the measured sweep)
+  uint64_t min_tiles_per_sm = 8;   // tiles <= nnz / (this x SMs) (DG_TILES_PER_SM)
   uint64_t tile_guide = 2;             // guided tail: tiles <= remaining / (guide * SMs) (0: off)
   uint64_t tile_guide_min = 64 * 1024;  // smallest guided tile (nonzeros)
   uint32_t n_waves = 0;

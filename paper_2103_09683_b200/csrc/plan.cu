@@ -390,7 +390,7 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
     std::vector<Segment>& segs = lsegs[lw];
     // ~8 tiles per SM at least in every launch (no single-tile tails), at most tile_nnz
     const uint64_t tile_nnz = std::max<uint64_t>(
-        4096, std::min<uint64_t>(h->tile_nnz, lnnz[lw] / (8ull * h->sm_count)));
+        4096, std::min<uint64_t>(h->tile_nnz, lnnz[lw] / (h->min_tiles_per_sm * h->sm_count)));
     // guided sizing: tiles are claimed in list order, so the kernel's tail is the duration of the
     // last tiles claimed.  Once the work left in the launch drops below ~guide tiles per SM,
     // tiles shrink with it (remaining / (guide * SMs)), down to guide_min nonzeros.
