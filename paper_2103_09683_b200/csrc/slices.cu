@@ -509,8 +509,11 @@ int launch_slices(Handle* h, const Acc* x, double* y, cudaStream_t s) {
 #define DG_SLICE_P_EXACT 2
 #endif
   constexpr int kP = std::is_same_v<Acc, float> ? 4 : DG_SLICE_P_EXACT;
-  auto kern = carry ? k_slices<Acc, Handle::kSliceWarpsCarry, kP, true>
-                    : k_slices<Acc, Handle::kSliceWarps, kP, false>;
+  // short segments (mean < 256 nonzeros, C1: 136): 4-chunk batches -- fewer chunks per batch
+  // behind each segment end
+  auto kern = carry                ? k_slices<Acc, Handle::kSliceWarpsCarry, kP, true>
+              : h->short_segments ? k_slices<Acc, Handle::kSliceWarps, kP, false, 2, 4>
+                                   : k_slices<Acc, Handle::kSliceWarps, kP, false>;
   const int warps = carry ? Handle::kSliceWarpsCarry : Handle::kSliceWarps;
   if (!h->tiles_attr) {
     DG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));

@@ -76,18 +76,20 @@ struct XGlob {
   __device__ __forceinline__ Acc operator[](uint32_t i) const { return __ldg(x + i); }
 };
 
-template <typename Acc, int P, bool CARRY, class XS = XSmem<Acc>>
+template <typename Acc, int P, bool CARRY, class XS = XSmem<Acc>, int U = kSliceU>
 __device__ __forceinline__ void run_slice(const uint4* __restrict__ blocks, uint32_t c0, uint32_t nblk,
                                           const SliceSeg* __restrict__ sseg, uint32_t s0,
                                           uint32_t s1, const XS xs, uint32_t neutral,
                                           const Carry<Acc>& carry, double* __restrict__ y,
                                           const GatherTargets& gt, uint32_t lane) {
   using Ops = AccOps<Acc>;
+  static_assert(U == 4 || U == 8, "a batch is one or two 4-chunk blocks");
+  constexpr uint32_t BL = U / kSliceBlock;  // blocks per batch
   if (nblk == 0) return;
-  // runs are padded to whole batches (kSlicePad = 8 chunks = 2 blocks): both blocks of every
-  // batch exist, so the loads need no guard and no neutral fill
-  static_assert(kSlicePad % (2 * kSliceBlock) == 0, "runs must hold whole batches");
-  const uint32_t nb = nblk / 2;  // batches
+  // runs are padded to whole batches (kSlicePad = 8 chunks = 2 blocks): every block of every
+  // batch exists, so the loads need no guard and no neutral fill
+  static_assert(kSlicePad % (BL * kSliceBlock) == 0, "runs must hold whole batches");
+  const uint32_t nb = nblk / BL;  // batches
   // current segment and the next one's descriptor (loaded one segment ahead)
   uint32_t si = s0;
   SliceSeg cur = sseg[si];
@@ -95,14 +97,17 @@ __device__ __forceinline__ void run_slice(const uint4* __restrict__ blocks, uint
   uint32_t left = cur.nch;
   Acc acc = CARRY ? carry.in(cur.slot, cur.flags, lane) : Acc(0);
   const uint4* p = blocks + static_cast<uint64_t>(c0 / 4) * 32 + lane;  // block c0/4, lane's 16 B
-  uint4 a0 = ld_stream16(p), a1 = ld_stream16(p + 32), b0, b1;
-  // L2 prefetch stream: lanes 0..7 each own one 128-byte line of a batch (1 KB), P batches ahead
+  uint4 a0 = ld_stream16(p), a1 = BL > 1 ? ld_stream16(p + 32) : a0, b0, b1;
+  // L2 prefetch stream: lanes 0 .. 4 BL - 1 each own one 128-byte line of a batch (512 BL bytes),
+  // P batches ahead
+  constexpr uint32_t kBatchBytes = 512 * BL;
   const char* pf = reinterpret_cast<const char*>(p - lane) + 128 * lane;
   if constexpr (P > 0) {
 #pragma unroll
     for (int k = 1; k <= P; ++k)
-      if (lane < 8 && static_cast<uint32_t>(k) < nb) asm volatile("prefetch.global.L2 [%0];" ::"l"(pf + 1024 * k));
-    pf += 1024 * (P + 1);
+      if (lane < 4 * BL && static_cast<uint32_t>(k) < nb)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(pf + kBatchBytes * k));
+    pf += kBatchBytes * (P + 1);
   }
   auto finish = [&]() {  // the current segment ends with the chunk just added
     if (!CARRY || (cur.flags & kSegLast)) {
@@ -127,66 +132,67 @@ __device__ __forceinline__ void run_slice(const uint4* __restrict__ blocks, uint
     }
   };
   auto consume = [&](const uint4& q0, const uint4& q1) {
-    const uint32_t r[kSliceU] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-    Acc xv[kSliceU];
+    const uint32_t r[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+    Acc xv[U];
 #pragma unroll
-    for (int k = 0; k < kSliceU; ++k) xv[k] = xs[r[k] >> 16];
-    if (left > static_cast<uint32_t>(kSliceU)) {  // the whole batch inside one segment
+    for (int k = 0; k < U; ++k) xv[k] = xs[r[k] >> 16];
+    if (left > static_cast<uint32_t>(U)) {  // the whole batch inside one segment
 #pragma unroll
-      for (int k = 0; k < kSliceU; ++k)
+      for (int k = 0; k < U; ++k)
         acc = Ops::add(acc, Ops::prod(static_cast<uint16_t>(r[k] & 0xFFFFu), xv[k]));
-      left -= kSliceU;
+      left -= U;
       return;
     }
     // segment end(s) inside the batch: the products once, then each segment's chunks [k, e)
     // added in position order under a warp-uniform bit mask, one finish() per segment end
-    Acc pr[kSliceU];
+    Acc pr[U];
 #pragma unroll
-    for (int j = 0; j < kSliceU; ++j) pr[j] = Ops::prod(static_cast<uint16_t>(r[j] & 0xFFFFu), xv[j]);
+    for (int j = 0; j < U; ++j) pr[j] = Ops::prod(static_cast<uint16_t>(r[j] & 0xFFFFu), xv[j]);
     uint32_t k = 0;
     do {
-      const uint32_t e = left >= kSliceU - k ? static_cast<uint32_t>(kSliceU) : k + left;
-      const uint32_t m = (0xFFu >> (kSliceU - (e - k))) << k;  // chunks k .. e-1
+      const uint32_t e = left >= U - k ? static_cast<uint32_t>(U) : k + left;
+      const uint32_t m = (0xFFu >> (8 - (e - k))) << k;  // chunks k .. e-1
 #pragma unroll
-      for (int j = 0; j < kSliceU; ++j)
+      for (int j = 0; j < U; ++j)
         if (m & (1u << j)) acc = Ops::add(acc, pr[j]);
       left -= e - k;
       k = e;
       if (left == 0) finish();
-    } while (k < static_cast<uint32_t>(kSliceU));
+    } while (k < static_cast<uint32_t>(U));
   };
+  constexpr uint32_t kStep = 32 * BL;  // uint4 per lane-major batch
   uint32_t bi = 0;
   for (;;) {
     // step A: consume a, load b
     if (bi + 1 < nb) {
-      b0 = ld_stream16(p + 64);
-      b1 = ld_stream16(p + 96);
+      b0 = ld_stream16(p + kStep);
+      if constexpr (BL > 1) b1 = ld_stream16(p + kStep + 32);
     }
     if constexpr (P > 0) {
-      if (lane < 8 && bi + 1 + P < nb) asm volatile("prefetch.global.L2 [%0];" ::"l"(pf));
-      pf += 1024;
+      if (lane < 4 * BL && bi + 1 + P < nb) asm volatile("prefetch.global.L2 [%0];" ::"l"(pf));
+      pf += kBatchBytes;
     }
     consume(a0, a1);
     if (++bi == nb) break;
-    p += 64;
+    p += kStep;
     // step B: consume b, load a
     if (bi + 1 < nb) {
-      a0 = ld_stream16(p + 64);
-      a1 = ld_stream16(p + 96);
+      a0 = ld_stream16(p + kStep);
+      if constexpr (BL > 1) a1 = ld_stream16(p + kStep + 32);
     }
     if constexpr (P > 0) {
-      if (lane < 8 && bi + 1 + P < nb) asm volatile("prefetch.global.L2 [%0];" ::"l"(pf));
-      pf += 1024;
+      if (lane < 4 * BL && bi + 1 + P < nb) asm volatile("prefetch.global.L2 [%0];" ::"l"(pf));
+      pf += kBatchBytes;
     }
     consume(b0, b1);
     if (++bi == nb) break;
-    p += 64;
+    p += kStep;
   }
 }
 
 // Persistent: one CTA per SM, NB x-window buffers of wcap elements (dynamic smem), element
 // wcap - 1 of each buffer is the zero slot the neutral words gather.
-template <typename Acc, int WARPS, int P, bool CARRY, int NB = 2>
+template <typename Acc, int WARPS, int P, bool CARRY, int NB = 2, int U = kSliceU>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     k_slices(const uint4* __restrict__ blocks, XSource<Acc> xsrc, const Tile* __restrict__ tiles,
              uint32_t n_tiles, uint32_t runs, const WarpRange* __restrict__ ranges,
@@ -303,9 +309,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       if (k >= runs) break;
       const WarpRange r0 = ranges[static_cast<uint64_t>(t) * runs + k];
       const WarpRange r1 = ranges[static_cast<uint64_t>(t) * runs + k + 1];
-      run_slice<Acc, P, CARRY>(blocks, r0.chunk, (r1.chunk - r0.chunk) / kSliceBlock, sseg, r0.seg,
-                               r1.seg, XSmem<Acc>{xbuf0 + b * wcap}, (wcap - 1) << 16, carry, y, gt,
-                               lane);
+      run_slice<Acc, P, CARRY, XSmem<Acc>, U>(blocks, r0.chunk, (r1.chunk - r0.chunk) / kSliceBlock, sseg,
+                                              r0.seg, r1.seg, XSmem<Acc>{xbuf0 + b * wcap}, (wcap - 1) << 16,
+                                              carry, y, gt, lane);
     }
     __syncwarp();
     if (lane == 0) {
