@@ -596,7 +596,7 @@ int launch_dense_slices(Handle* h, const Acc* x, double* y, cudaStream_t s) {
   k_dense_slices<Acc, kP><<<grid, 256, 0, s>>>(
       reinterpret_cast<const uint4*>(h->d_dslices), static_cast<const WarpRange*>(h->d_dranges),
       static_cast<const SliceSeg*>(h->d_dsseg), static_cast<uint32_t>(h->n_dense_rows), x,
-      static_cast<uint32_t>(h->cols) << 16, h->d_dense_counter, y, h->gt);
+      h->d_dense_counter, y, h->gt);
   h->post(s, "dense", h->n_dense_rows, h->dense_nnz);
   DG_CUDA(cudaGetLastError());
   return DG_OK;

@@ -16,7 +16,7 @@
 //     8 chunks is two fully coalesced LDG.128 per lane, aligned to 128-byte lines.
 // Compared with the row-ordered stream (k_tiles): no segment-edge lines fetched twice (adjacent
 // rows of the row-ordered stream sit in unrelated tiles), no misaligned 2-line chunk requests, no
-// masked edge batches; the price is the neutral padding (< 32 words per segment end, < 4 chunks
+// masked edge batches; the price is the neutral padding (< 32 words per segment end, < 8 chunks
 // per run).  Results are bit-identical: each lane adds the same products in the same
 // order from +0.0, and a neutral word adds +0 * (+0.0) = +0.0, the identity of an accumulator
 // that is never -0.0.
@@ -79,8 +79,7 @@ struct XGlob {
 template <typename Acc, int P, bool CARRY, class XS = XSmem<Acc>, int U = kSliceU>
 __device__ __forceinline__ void run_slice(const uint4* __restrict__ blocks, uint32_t c0, uint32_t nblk,
                                           const SliceSeg* __restrict__ sseg, uint32_t s0,
-                                          uint32_t s1, const XS xs, uint32_t neutral,
-                                          const Carry<Acc>& carry, double* __restrict__ y,
+                                          uint32_t s1, const XS xs, const Carry<Acc>& carry, double* __restrict__ y,
                                           const GatherTargets& gt, uint32_t lane) {
   using Ops = AccOps<Acc>;
   static_assert(U == 4 || U == 8, "a batch is one or two 4-chunk blocks");
@@ -310,8 +309,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       const WarpRange r0 = ranges[static_cast<uint64_t>(t) * runs + k];
       const WarpRange r1 = ranges[static_cast<uint64_t>(t) * runs + k + 1];
       run_slice<Acc, P, CARRY, XSmem<Acc>, U>(blocks, r0.chunk, (r1.chunk - r0.chunk) / kSliceBlock, sseg,
-                                              r0.seg, r1.seg, XSmem<Acc>{xbuf0 + b * wcap}, (wcap - 1) << 16,
-                                              carry, y, gt, lane);
+                                              r0.seg, r1.seg, XSmem<Acc>{xbuf0 + b * wcap}, carry, y,
+                                              gt, lane);
     }
     __syncwarp();
     if (lane == 0) {
@@ -361,7 +360,7 @@ template <typename Acc, int P>
 __global__ void __launch_bounds__(256)
     k_dense_slices(const uint4* __restrict__ blocks, const WarpRange* __restrict__ ranges,
                    const SliceSeg* __restrict__ sseg, uint32_t n_rows, const Acc* __restrict__ x,
-                   uint32_t neutral, uint32_t* __restrict__ counter, double* __restrict__ y,
+                   uint32_t* __restrict__ counter, double* __restrict__ y,
                    const __grid_constant__ GatherTargets gt) {
   // programmatic dependent launch: the tile kernel that follows may take each SM as soon as this
   // grid's CTAs there have exited (it touches other rows)
@@ -375,7 +374,7 @@ __global__ void __launch_bounds__(256)
     if (k >= n_rows) break;
     const uint32_t c0 = ranges[k].chunk, c1 = ranges[k + 1].chunk;
     run_slice<Acc, P, false>(blocks, c0, (c1 - c0) / kSliceBlock, sseg, k, k + 1, XGlob<Acc>{x},
-                             neutral, no_carry, y, gt, lane);
+                             no_carry, y, gt, lane);
   }
 }
 
