@@ -160,7 +160,8 @@ int dg_dose(dg_handle* h, const double* x, uint64_t x_len, double* y, uint32_t f
  * each target -- the full-d buffers of all ranks (this rank's included), mapped into this
  * process through CUDA IPC (dg_ipc_*) -- at global row row_begin + r: the dose kernels' epilogues
  * store each finished row to every target (P2P stores over NVLink, overlapped with the rest of
- * the kernel), and this shard's row range of every target is zero-filled first (its empty rows).
+ * the kernel); this shard's row range of every target is zero-filled by the first dose after
+ * the call (its empty rows, which no later dose writes: the targets are read-only to callers).
  * When every rank's dose has completed (the caller's barrier), every rank holds the full d: the
  * all-gather costs no separate collective.  targets == NULL / n == 0 disables. */
 int dg_set_gather_targets(dg_handle* h, double* const* targets, uint32_t n);

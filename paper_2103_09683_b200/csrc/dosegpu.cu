@@ -405,9 +405,14 @@ int run_kernels(Handle* h, const double* d_x, double* d_y, cudaStream_t s) {
   h->n_launch = 0;
   if (h->rows) DG_CUDA(cudaMemsetAsync(d_y, 0, h->rows * sizeof(double), s));
   // fused gather: this shard's rows of every rank's full d start at +0.0 (its empty rows); the
-  // kernels then store each finished row into every target over NVLink
-  for (uint32_t i = 0; i < h->gt.n && h->rows; ++i)
-    DG_CUDA(cudaMemsetAsync(h->gt.t[i] + h->gt.row_off, 0, h->rows * sizeof(double), s));
+  // kernels then store each finished row into every target over NVLink.  Once per target list:
+  // no kernel ever writes an empty row, so later doses find them still +0.0 (the full-d buffers
+  // are the library's, read-only to the caller) -- no rows x targets x 8 B of remote zeroes per dose
+  if (!h->gt_zeroed) {
+    for (uint32_t i = 0; i < h->gt.n && h->rows; ++i)
+      DG_CUDA(cudaMemsetAsync(h->gt.t[i] + h->gt.row_off, 0, h->rows * sizeof(double), s));
+    h->gt_zeroed = true;
+  }
   if (h->profiling) DG_CUDA(cudaEventRecord(h->kev[0], s));
   int st;
   if (h->accumulation == DG_ACCUM_FP32) {

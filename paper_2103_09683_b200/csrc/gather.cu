@@ -28,6 +28,7 @@ int dg_set_gather_targets(dg_handle* hh, double* const* targets, uint32_t n) {
   gt.n = n;
   gt.row_off = h->row_begin;
   h->gt = gt;
+  h->gt_zeroed = false;  // the next dose zero-fills this shard's rows of the new targets
   return DG_OK;
 }
 

@@ -139,6 +139,7 @@ struct Handle {
 
   // fused d gather: every finished row also goes to each rank's full-d buffer (peer memory)
   GatherTargets gt = {};
+  bool gt_zeroed = false;  // this shard's rows of every target were zero-filled (once per list)
 
   // staging for host x / y and the fp32 family
   // x staged for the tile kernel (XSource): d_x_raw + kXPad is x (16-byte aligned, 16 readable

@@ -199,7 +199,8 @@ class FusedGather:
 
     def dose(self, x, y_local, *, stream: int = 0):
         """This rank's slice into y_local and into every rank's full d; returns this rank's full
-        d once every rank has finished (stream sync + barrier).  The returned tensor is valid
+        d once every rank has finished (stream sync + barrier).  The returned tensor is read-only
+        (its empty rows are zero-filled once, at the first dose, and never rewritten) and valid
         until the next ``dose`` call: that call first waits at a barrier for every rank (so no
         rank is still reading its full d from the previous dose when the peers' kernels start
         overwriting it), then overwrites it."""
