@@ -403,7 +403,12 @@ int launch_fp32(Handle* h, const M& mat, const float* x, double* y, cudaStream_t
 
 int run_kernels(Handle* h, const double* d_x, double* d_y, cudaStream_t s) {
   h->n_launch = 0;
-  if (h->rows) DG_CUDA(cudaMemsetAsync(d_y, 0, h->rows * sizeof(double), s));
+  // empty rows are +0.0 (spmv.cpp:56): the caller's device d every dose; the handle's own d (host
+  // path) once -- no kernel writes an empty row
+  if (h->rows && (d_y != h->d_y || !h->dy_zeroed)) {
+    DG_CUDA(cudaMemsetAsync(d_y, 0, h->rows * sizeof(double), s));
+    if (d_y == h->d_y) h->dy_zeroed = true;
+  }
   // fused gather: this shard's rows of every rank's full d start at +0.0 (its empty rows); the
   // kernels then store each finished row into every target over NVLink.  Once per target list:
   // no kernel ever writes an empty row, so later doses find them still +0.0 (the full-d buffers

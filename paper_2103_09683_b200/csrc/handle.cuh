@@ -150,6 +150,7 @@ struct Handle {
   double* d_x = nullptr;   // = d_x_raw + kXPad
   double* d_x1 = nullptr;  // = d_x1_raw + kXPad + 1
   double* d_y = nullptr;
+  bool dy_zeroed = false;  // d_y's empty rows hold +0.0 (zero-filled by the first host-d dose)
   float* d_xf = nullptr;
   unsigned* d_bad = nullptr;
 
