@@ -56,7 +56,8 @@ struct Handle {
   uint64_t slot_tiles = 0;         // slot-mode tiles in the plan
   bool slots_encoded = false;      // the stream's slot-mode positions hold slots (else columns)
   // slice stream (spmv_slices.cuh, slices.cu): binary16 matrices under lane_width 32
-  static constexpr int kSliceWarps = 32;       // warps per CTA of k_slices
+  static constexpr int kSliceWarps = 28;       // warps per CTA of k_slices (72 registers; r02: 28 / 32 / 24 warps: C2 1.214 / 1.219 / 1.275 ms, C3 shard 0.176 / 0.182, C5 and 100-step C2 -1 to -5%)
+  static constexpr int kSliceWarpsShort = 32;  // ... with 4-chunk batches (short segments; C1: 32 / 28 warps 0.0996 / 0.1036 ms)
   static constexpr int kSliceWarpsCarry = 28;  // ... with carried partials (r02 C4: 20 / 24 / 26 / 28 / 32 warps 4.11 / 3.79 / 3.79 / 3.66 / 4.34 ms; 28 = 72 registers)
   bool slices_wanted = false;      // plan for the slice stream (DG_SLICES=0: row-ordered k_tiles)
   bool slices = false;             // the plan has one; d_slices holds it

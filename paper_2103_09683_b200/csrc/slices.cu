@@ -22,7 +22,8 @@ namespace dg {
 // warp time waiting on a window on C2's 1/8 shard (DG_TRACE).  Each run is padded to whole
 // 8-chunk batches (two 512-byte blocks), so the kernel's loads need no guards.
 int plan_slices(Handle* h, const std::vector<Tile>& tiles, std::vector<Segment>& segs) {
-  const int WARPS = h->n_carry_slots ? Handle::kSliceWarpsCarry : Handle::kSliceWarps;
+  const int WARPS = h->n_carry_slots ? Handle::kSliceWarpsCarry
+                    : h->short_segments ? Handle::kSliceWarpsShort : Handle::kSliceWarps;
   int RUNS = WARPS * Handle::kRunsPerWarp;
   if (const char* rw = std::getenv("DG_RUNS_PER_WARP")) RUNS = WARPS * std::max(1, std::atoi(rw));
   std::vector<WarpRange> R;
@@ -512,9 +513,10 @@ int launch_slices(Handle* h, const Acc* x, double* y, cudaStream_t s) {
   // short segments (mean < 256 nonzeros, C1: 136): 4-chunk batches -- fewer chunks per batch
   // behind each segment end
   auto kern = carry                ? k_slices<Acc, Handle::kSliceWarpsCarry, kP, true>
-              : h->short_segments ? k_slices<Acc, Handle::kSliceWarps, kP, false, 2, 4>
+              : h->short_segments ? k_slices<Acc, Handle::kSliceWarpsShort, kP, false, 2, 4>
                                    : k_slices<Acc, Handle::kSliceWarps, kP, false>;
-  const int warps = carry ? Handle::kSliceWarpsCarry : Handle::kSliceWarps;
+  const int warps = carry ? Handle::kSliceWarpsCarry
+                    : h->short_segments ? Handle::kSliceWarpsShort : Handle::kSliceWarps;
   if (!h->tiles_attr) {
     DG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     h->tiles_attr = true;
