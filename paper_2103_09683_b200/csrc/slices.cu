@@ -507,7 +507,7 @@ int launch_slices(Handle* h, const Acc* x, double* y, cudaStream_t s) {
   const size_t smem = 2ull * h->window_cols * sizeof(Acc);
   const bool carry = h->n_carry_slots != 0;
 #ifndef DG_SLICE_P_EXACT
-#define DG_SLICE_P_EXACT 2
+#define DG_SLICE_P_EXACT 3  // r02 at 28 warps: P = 2 / 3 / 4: C2 slices 1.229 / 1.211 / 1.210 ms, C4 3.546 / 3.509
 #endif
   constexpr int kP = std::is_same_v<Acc, float> ? 4 : DG_SLICE_P_EXACT;
   // short segments (mean < 256 nonzeros, C1: 136): 4-chunk batches -- fewer chunks per batch
