@@ -494,6 +494,8 @@ int finish_create(Handle* h, const std::vector<uint64_t>& lens) {
   DG_CUDA(cudaEventCreateWithFlags(&h->ev_tiles_start, cudaEventDisableTiming));
   DG_CUDA(cudaEventCreateWithFlags(&h->ev_d2h_done, cudaEventDisableTiming));
   DG_CUDA(cudaStreamCreateWithFlags(&h->d2h_stream, cudaStreamNonBlocking));
+  DG_CUDA(cudaStreamCreateWithFlags(&h->d2h_stream2, cudaStreamNonBlocking));
+  DG_CUDA(cudaEventCreateWithFlags(&h->ev_d2h_done2, cudaEventDisableTiming));
   // create-time work (memsets, plan uploads, setup kernels) ran on the legacy stream, which the
   // handle's non-blocking dose streams do not wait on: finish it before the handle is returned
   DG_CUDA(cudaDeviceSynchronize());
@@ -688,6 +690,11 @@ int dg_destroy(dg_handle* hh) {
     cudaStreamSynchronize(h->d2h_stream);
     cudaStreamDestroy(h->d2h_stream);
   }
+  if (h->d2h_stream2) {
+    cudaStreamSynchronize(h->d2h_stream2);
+    cudaStreamDestroy(h->d2h_stream2);
+  }
+  if (h->ev_d2h_done2) cudaEventDestroy(h->ev_d2h_done2);
   if (h->ev_tiles_start) cudaEventDestroy(h->ev_tiles_start);
 
   if (h->ev_d2h_done) cudaEventDestroy(h->ev_d2h_done);
@@ -746,22 +753,30 @@ int dg_dose(dg_handle* hh, const double* x, uint64_t x_len, double* y, uint32_t 
   DG_TRY(dg::run_kernels(h, d_x, d_y, s));
   DG_CUDA(cudaEventRecord(h->ev[2], s));
   if (overlap) {
-    DG_CUDA(cudaStreamWaitEvent(h->d2h_stream, h->ev_tiles_start, 0));
-
+    // blocks alternate between two copy streams (two copy engines: DG_D2H_STREAMS=1 for one)
+    static const int n_d2h = [] { const char* v = std::getenv("DG_D2H_STREAMS"); return v && *v == '1' ? 1 : 2; }();
+    cudaStream_t cs[2] = {h->d2h_stream, n_d2h > 1 ? h->d2h_stream2 : h->d2h_stream};
+    DG_CUDA(cudaStreamWaitEvent(cs[0], h->ev_tiles_start, 0));
+    if (cs[1] != cs[0]) DG_CUDA(cudaStreamWaitEvent(cs[1], h->ev_tiles_start, 0));
     for (uint32_t k = 0; k < h->n_blocks; ++k) {
       const uint64_t r0 = h->blk_row0[k], r1 = h->blk_row0[k + 1];
       if (r1 == r0) continue;
+      cudaStream_t c = cs[k & 1];
       if (h->blk_tiles[k]) {
         const CUresult cr = dg::wait_value_fn()(
-            reinterpret_cast<CUstream>(h->d2h_stream),
+            reinterpret_cast<CUstream>(c),
             reinterpret_cast<CUdeviceptr>(h->d_blk_flag + k), h->epoch, CU_STREAM_WAIT_VALUE_GEQ);
         if (cr != CUDA_SUCCESS) return DG_ERR_CUDA_BASE + static_cast<int>(cudaErrorUnknown);
       }
       DG_CUDA(cudaMemcpyAsync(y + r0, h->d_y + r0, (r1 - r0) * sizeof(double),
-                              cudaMemcpyDeviceToHost, h->d2h_stream));
+                              cudaMemcpyDeviceToHost, c));
     }
-    DG_CUDA(cudaEventRecord(h->ev_d2h_done, h->d2h_stream));
+    DG_CUDA(cudaEventRecord(h->ev_d2h_done, cs[0]));
     DG_CUDA(cudaStreamWaitEvent(s, h->ev_d2h_done, 0));
+    if (cs[1] != cs[0]) {
+      DG_CUDA(cudaEventRecord(h->ev_d2h_done2, cs[1]));
+      DG_CUDA(cudaStreamWaitEvent(s, h->ev_d2h_done2, 0));
+    }
   } else if (!y_dev && h->rows) {
     DG_CUDA(cudaMemcpyAsync(y, h->d_y, h->rows * sizeof(double), cudaMemcpyDeviceToHost, s));
   }

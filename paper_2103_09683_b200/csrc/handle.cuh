@@ -134,7 +134,8 @@ struct Handle {
   uint32_t* d_blk_left_init = nullptr;  // the tile counts, copied into d_blk_left per dose
   uint32_t* d_blk_flag = nullptr;       // epoch of the dose that last completed block k
   uint32_t epoch = 0;
-  cudaStream_t d2h_stream = nullptr;
+  cudaStream_t d2h_stream = nullptr, d2h_stream2 = nullptr;
+  cudaEvent_t ev_d2h_done2 = nullptr;
   cudaEvent_t ev_tiles_start = nullptr, ev_d2h_done = nullptr;
   bool signal_blocks = false;  // this dose publishes block completion (host d, overlapped D2H)
 
