@@ -109,6 +109,7 @@ def test_ddm_row_shards_read_only_their_ranges(ref, port, tmp_path, parts):
         with dg.DoseEngine.from_ddm(p, row_begin=r0, row_end=r1) as e:
             assert (e.info["row_begin"], e.info["row_end"], e.info["rows"]) == (r0, r1, r1 - r0)
             assert e.info["nnz"] == int(m.row_ptr[r1] - m.row_ptr[r0])
+            assert e.info["read_ns"] > 0  # the reader's own time (sections -> device)
             # resident bytes are the shard's, not the file's
             assert e.info["device_bytes"] < 1.5 * (e.info["nnz"] * 4 + 8 * (r1 - r0)) + (8 << 20)
             got[r0:r1] = e.dose(x)
