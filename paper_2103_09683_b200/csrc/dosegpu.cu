@@ -751,7 +751,12 @@ int dg_dose(dg_handle* hh, const double* x, uint64_t x_len, double* y, uint32_t 
   //  with the slice kernel: 4.82 vs 4.59 ms, and 4.78-4.83 with wave lags 1 / 2 / 4).
   // (measured, rejected: with pinned host d, running the contiguous rows LAST -- after the block
   //  downloads, storing their rows into the pinned d zero-copy -- C2 end to end 2.10 vs 2.10 ms:
-  //  the 64 MB download runs at ~45 GB/s beside the kernels either way, 1.42 ms)
+  //  the 64 MB download runs at ~45 GB/s beside the kernels either way, 1.42 ms.  Measured again
+  //  in its concurrent form -- the contiguous rows right after the tile kernel, each row stored
+  //  into the mapped host d once its block's download is flagged done (cuStreamWriteValue32):
+  //  e2e 1.922-1.928 vs 1.930-1.932 ms values-first, 32 / 64 blocks 2.00 / 2.10; the PCIe
+  //  download beside the HBM-bound kernels (34-44 GB/s; 53.7 GB/s on an idle GPU,
+  //  scripts/micro/pcie_d2h.cu) bounds the end-to-end step either way)
   const bool overlap = !y_dev && h->rows && h->use_tiles && h->n_waves == 1 &&
                        h->n_blocks > 1 && dg::wait_value_fn() && !(no_ovl && *no_ovl == '1');
   h->signal_blocks = overlap;

@@ -84,6 +84,30 @@ def test_c4_full_vector_exact(port):
             _full_vector_match(port, e, x, e.dose(x))
 
 
+@pytest.mark.parametrize("blocks", ["16", "64"])
+def test_c2_pinned_host_path_alternating_x(monkeypatch, blocks):
+    """The end-to-end path bench.py times: pinned host x and d, each row block downloaded as soon
+    as the tile kernel flags its last tile done (cuStreamWaitValue32), while later blocks are still
+    computed.  x alternates between doses, so a block downloaded before its rows were final would
+    show the previous dose's values; every dose's host d is bit-identical to the device-resident d
+    of the same x (itself pinned to the oracle by test_c2_full_vector_exact_and_fp32)."""
+    import torch
+    monkeypatch.setenv("DG_BLOCKS", blocks)
+    p = dg.profiles.c2()
+    xs = [dg.seeded_vector(p.cols, 42), dg.seeded_vector(p.cols, 43)]
+    with dg.DoseEngine.generate(p) as e:
+        want = []
+        for x in xs:
+            yd = torch.empty(p.rows, dtype=torch.float64, device="cuda")
+            e.dose_device(torch.from_numpy(x).cuda().data_ptr(), p.cols, yd.data_ptr())
+            want.append(yd.cpu())
+        xh = [torch.from_numpy(x).pin_memory() for x in xs]
+        yh = torch.full((p.rows,), 7.0, dtype=torch.float64).pin_memory()
+        for it in range(8):
+            e.dose_host_ptrs(xh[it % 2].data_ptr(), p.cols, yh.data_ptr())
+            assert torch.equal(yh.view(torch.int64), want[it % 2].view(torch.int64)), it
+
+
 @pytest.mark.parametrize("G", [8])
 def test_c3_shards_concatenate_to_the_single_gpu_dose(G):
     """Each rank's nnz-balanced row shard of C2 (exactly what bench.py --gpus G gives it; the

@@ -692,6 +692,15 @@ def test_contiguous_rows_values_only_bit_exact(port, monkeypatch, min_len, iw):
             e.dose_host_ptrs(xh.data_ptr(), m.cols, yh.data_ptr())
             assert np.array_equal(yh.numpy().view(np.uint64), want)
             yh.fill_(7.0)
+        # alternating x on the pinned path: a block downloaded before its last tile finished
+        # would keep the previous dose's values
+        x2 = x * 2.0
+        want2 = bits(port.spmv_rowchunk(m, x2, 32, 2))
+        x2h = torch.from_numpy(x2).pin_memory()
+        for it in range(6):
+            xx, ww = (xh, want) if it % 2 == 0 else (x2h, want2)
+            e.dose_host_ptrs(xx.data_ptr(), m.cols, yh.data_ptr())
+            assert np.array_equal(yh.numpy().view(np.uint64), ww)
         back = e.copy_rows(0, m.rows)
         assert np.array_equal(back.row_ptr, m.row_ptr)
         assert np.array_equal(back.col_indices, m.col)
