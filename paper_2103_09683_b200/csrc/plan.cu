@@ -193,10 +193,22 @@ int plan_tiles_typed(Handle* h, const M& mat, const std::vector<uint64_t>& lens)
   h->dense_kernel = h->dense_mode != 0 && (dense_all || 100 * wide_dense >= h->nnz || (slices && wide_dense));
   // contiguous rows >= dense_min_len go to k_dense_values whenever the slice stream is planned
   // (binary16 values under lane width 32): their column words are implied, half the bytes
-  auto contiguous = [&](uint64_t r) {
+  auto contiguous_row = [&](uint64_t r) {
     return slices && h->dense_mode != 0 && lens[r] >= h->dense_min_len && lens[r] > h->short_max &&
            static_cast<uint64_t>(ext[r].y) - ext[r].x + 1 == lens[r];
   };
+  // Auto: only when they are >= 0.5% of the nonzeros.  A handful of them (C1: 16 rows of 4,096,
+  // 0.16%) leaves k_dense_values one latency-bound row per warp (~12 us for 4,096 positions) that
+  // the tile kernel's CTAs wait behind; in the tiles they cost nothing (C1 0.118 -> 0.114 ms).
+  // C2 / C3 / C5: 42%, C4: 1.0%.
+  bool values_on = h->dense_mode > 0;
+  if (h->dense_mode < 0 && slices) {
+    uint64_t cnnz = 0;
+    for (uint64_t r = 0; r < rows; ++r)
+      if (contiguous_row(r)) cnnz += lens[r];
+    values_on = 200 * cnnz >= h->nnz;
+  }
+  auto contiguous = [&](uint64_t r) { return values_on && contiguous_row(r); };
   if (!h->dense_kernel)
     for (uint64_t r = 0; r < rows && !h->dense_kernel; ++r) h->dense_kernel = contiguous(r);
   std::vector<std::vector<HostSeg>> waves(1);
