@@ -30,7 +30,9 @@ struct Row {
 };
 
 // values: lane-major 8-chunk blocks (512 B: lane l's 16 B = its 8 halves); batch = 2 blocks
-template <int P>
+// AL: x read from the row's 32-element-aligned base (lo & ~31) -- the traffic of a lane grid
+// rotated by lo mod 32 (each chunk's 32 x elements in 2 aligned 128-B lines instead of 3)
+template <int P, bool AL = false>
 __global__ void __launch_bounds__(256) k_values(const uint4* __restrict__ s, const Row* __restrict__ rows,
                                                 uint32_t n_rows, const double* __restrict__ x,
                                                 uint32_t zero_col, uint32_t* counter, double* y) {
@@ -60,7 +62,7 @@ __global__ void __launch_bounds__(256) k_values(const uint4* __restrict__ s, con
       if (pos0 + 15 * 32 < R.len) {  // interior batch: all 16 positions inside the row
         double xv[16];
 #pragma unroll
-        for (int c = 0; c < 16; ++c) xv[c] = __ldg(x + R.lo + pos0 + 32 * c);
+        for (int c = 0; c < 16; ++c) xv[c] = __ldg(x + (AL ? R.lo & ~31u : R.lo) + pos0 + 32 * c);
 #pragma unroll
         for (int c = 0; c < 16; ++c) acc = __dadd_rn(acc, __dmul_rn(h2d(w[c / 2] >> (16 * (c & 1))), xv[c]));
       } else {
@@ -68,7 +70,7 @@ __global__ void __launch_bounds__(256) k_values(const uint4* __restrict__ s, con
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
           const uint32_t pos = pos0 + 32 * c;
-          xv[c] = __ldg(x + (pos < R.len ? R.lo + pos : zero_col));
+          xv[c] = __ldg(x + (pos < R.len ? (AL ? R.lo & ~31u : R.lo) + pos : zero_col));
         }
 #pragma unroll
         for (int c = 0; c < 16; ++c) acc = __dadd_rn(acc, __dmul_rn(h2d(w[c / 2] >> (16 * (c & 1))), xv[c]));
@@ -215,6 +217,12 @@ int main(int argc, char** argv) {
     time(nm, [&] { k_values<2><<<g * sms, 256>>>(sv, drv, n, x, cols, cnt, y); }, off_v * 16.0);
     snprintf(nm, sizeof nm, "values (2 B) P4 grid %dxSM", g);
     time(nm, [&] { k_values<4><<<g * sms, 256>>>(sv, drv, n, x, cols, cnt, y); }, off_v * 16.0);
+    snprintf(nm, sizeof nm, "values aligned-x P2 grid %dxSM", g);
+    time(nm, [&] { k_values<2, true><<<g * sms, 256>>>(sv, drv, n, x, cols, cnt, y); }, off_v * 16.0);
+    snprintf(nm, sizeof nm, "values (2 B) P2 grid %dxSM", g);
+    time(nm, [&] { k_values<2><<<g * sms, 256>>>(sv, drv, n, x, cols, cnt, y); }, off_v * 16.0);
+    snprintf(nm, sizeof nm, "values aligned-x P2 grid %dxSM", g);
+    time(nm, [&] { k_values<2, true><<<g * sms, 256>>>(sv, drv, n, x, cols, cnt, y); }, off_v * 16.0);
   }
   return 0;
 }
