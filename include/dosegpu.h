@@ -166,6 +166,16 @@ int dg_dose(dg_handle* h, const double* x, uint64_t x_len, double* y, uint32_t f
  * all-gather costs no separate collective.  targets == NULL / n == 0 disables. */
 int dg_set_gather_targets(dg_handle* h, double* const* targets, uint32_t n);
 
+/* The same exchange by the copy engines instead of the kernels' epilogues: with n targets set,
+ * every dg_dose copies this shard's d into each target (at global row row_begin + r) row block by
+ * row block -- block k as soon as the tile kernel publishes that its last tile is done
+ * (cuStreamWaitValue32 on the block's flag), while the kernel works on later blocks -- in
+ * coalesced DMA transfers over NVLink / NVSwitch that cost no SM time (plans without row blocks:
+ * right after the kernels).  The copies complete before the dose does on its stream.  Replaces
+ * the serial join of ddm::spmv_rowchunk's parallel_blocks (src/spmv.cpp:17-32) across GPUs.
+ * targets == NULL / n == 0 disables; may be combined with dg_set_gather_targets. */
+int dg_set_block_targets(dg_handle* h, double* const* targets, uint32_t n);
+
 /* Minimal CUDA IPC plumbing for the targets (64-byte cudaIpcMemHandle_t). */
 int dg_ipc_alloc(uint64_t bytes, int32_t device, void** dptr, void* handle64);
 int dg_ipc_open(const void* handle64, int32_t device, void** dptr);

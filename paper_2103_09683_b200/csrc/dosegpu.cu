@@ -509,6 +509,28 @@ int finish_create(Handle* h, const std::vector<uint64_t>& lens) {
 }
 
 // cuStreamWaitValue32 through the runtime's driver entry-point query (no libcuda link needed).
+bool set_block_sinks(Handle* h, const double* const* dst, const int* dev, uint32_t n) {
+  h->sink_ptr.assign(const_cast<double* const*>(dst), const_cast<double* const*>(dst) + n);
+  h->sink_dev.assign(dev, dev + n);
+  h->sink_remote = false;  // a sink on another device (or a UVA / IPC mapping: assumed remote)
+  for (uint32_t i = 0; i < n; ++i) h->sink_remote |= dev[i] < 0 || dev[i] != h->device;
+  return true;
+}
+
+// rows [r0, r1) of this shard's d (src: device) into every sink: peer copies between devices of
+// this process (dg_multi), plain UVA copies for CUDA-IPC mappings (sink_dev < 0)
+int copy_to_sinks(Handle* h, const double* src, uint64_t r0, uint64_t r1, cudaStream_t c) {
+  for (size_t i = 0; i < h->sink_ptr.size() && r1 > r0; ++i) {
+    if (h->sink_dev[i] >= 0)
+      DG_CUDA(cudaMemcpyPeerAsync(h->sink_ptr[i] + r0, h->sink_dev[i], src + r0, h->device,
+                                  (r1 - r0) * sizeof(double), c));
+    else
+      DG_CUDA(cudaMemcpyAsync(h->sink_ptr[i] + r0, src + r0, (r1 - r0) * sizeof(double),
+                              cudaMemcpyDefault, c));
+  }
+  return DG_OK;
+}
+
 WaitValueFn wait_value_fn() {
   static const WaitValueFn fn = [] {
     void* p = nullptr;
@@ -757,10 +779,19 @@ int dg_dose(dg_handle* hh, const double* x, uint64_t x_len, double* y, uint32_t 
   //  e2e 1.922-1.928 vs 1.930-1.932 ms values-first, 32 / 64 blocks 2.00 / 2.10; the PCIe
   //  download beside the HBM-bound kernels (34-44 GB/s; 53.7 GB/s on an idle GPU,
   //  scripts/micro/pcie_d2h.cu) bounds the end-to-end step either way)
-  const bool overlap = !y_dev && h->rows && h->use_tiles && h->n_waves == 1 &&
-                       h->n_blocks > 1 && dg::wait_value_fn() && !(no_ovl && *no_ovl == '1');
-  h->signal_blocks = overlap;
-  if (overlap) ++h->epoch;
+  const bool block_plan = h->rows && h->use_tiles && h->n_waves == 1 && h->n_blocks > 1 &&
+                          dg::wait_value_fn() && !(no_ovl && *no_ovl == '1');
+  const bool overlap = !y_dev && block_plan;
+  // dg_multi PEER gather (device d): each block copied to the other devices' full d as it completes
+  // (only toward other devices: copies into this device's own memory would compete with the
+  //  kernels for the same HBM -- dg_multi on a virtual device list {0,0,0,0}: 2.12 ms overlapped
+  //  vs 1.98 after the kernels; DG_SINK_OVERLAP=1 forces it for tests)
+  const char* fs = std::getenv("DG_SINK_OVERLAP");
+  const bool force_sink = fs && *fs == '1';
+  h->sink_overlap = y_dev && block_plan && !h->sink_ptr.empty() && !h->profiling &&
+                    (h->sink_remote || force_sink);
+  h->signal_blocks = overlap || h->sink_overlap;
+  if (h->signal_blocks) ++h->epoch;
   DG_TRY(dg::run_kernels(h, d_x, d_y, s));
   DG_CUDA(cudaEventRecord(h->ev[2], s));
   if (overlap) {
@@ -781,6 +812,7 @@ int dg_dose(dg_handle* hh, const double* x, uint64_t x_len, double* y, uint32_t 
       }
       DG_CUDA(cudaMemcpyAsync(y + r0, h->d_y + r0, (r1 - r0) * sizeof(double),
                               cudaMemcpyDeviceToHost, c));
+      DG_TRY(dg::copy_to_sinks(h, h->d_y, r0, r1, c));
     }
     DG_CUDA(cudaEventRecord(h->ev_d2h_done, cs[0]));
     DG_CUDA(cudaStreamWaitEvent(s, h->ev_d2h_done, 0));
@@ -790,6 +822,40 @@ int dg_dose(dg_handle* hh, const double* x, uint64_t x_len, double* y, uint32_t 
     }
   } else if (!y_dev && h->rows) {
     DG_CUDA(cudaMemcpyAsync(y, h->d_y, h->rows * sizeof(double), cudaMemcpyDeviceToHost, s));
+    DG_TRY(dg::copy_to_sinks(h, h->d_y, 0, h->rows, s));
+  } else if (y_dev && h->rows && !h->sink_ptr.empty()) {
+    // dg_multi PEER gather: block k of this shard's d goes to every other device's full d as
+    // soon as its last tile is done (sink_overlap), or all of it after the kernels
+    static const int n_cs = [] { const char* v = std::getenv("DG_D2H_STREAMS"); return v && *v == '1' ? 1 : 2; }();
+    cudaStream_t cs[2] = {h->d2h_stream, n_cs > 1 ? h->d2h_stream2 : h->d2h_stream};
+    if (h->sink_overlap) {
+      DG_CUDA(cudaStreamWaitEvent(cs[0], h->ev_tiles_start, 0));
+      if (cs[1] != cs[0]) DG_CUDA(cudaStreamWaitEvent(cs[1], h->ev_tiles_start, 0));
+    } else {
+      DG_CUDA(cudaEventRecord(h->ev_tiles_start, s));  // (after the kernels)
+      DG_CUDA(cudaStreamWaitEvent(cs[0], h->ev_tiles_start, 0));
+      if (cs[1] != cs[0]) DG_CUDA(cudaStreamWaitEvent(cs[1], h->ev_tiles_start, 0));
+    }
+    const uint32_t nb = h->sink_overlap ? h->n_blocks : 1;
+    for (uint32_t k = 0; k < nb; ++k) {
+      const uint64_t r0 = h->sink_overlap ? h->blk_row0[k] : 0;
+      const uint64_t r1 = h->sink_overlap ? h->blk_row0[k + 1] : h->rows;
+      if (r1 == r0) continue;
+      cudaStream_t c = cs[k & 1];
+      if (h->sink_overlap && h->blk_tiles[k]) {
+        const CUresult cr = dg::wait_value_fn()(
+            reinterpret_cast<CUstream>(c),
+            reinterpret_cast<CUdeviceptr>(h->d_blk_flag + k), h->epoch, CU_STREAM_WAIT_VALUE_GEQ);
+        if (cr != CUDA_SUCCESS) return DG_ERR_CUDA_BASE + static_cast<int>(cudaErrorUnknown);
+      }
+      DG_TRY(dg::copy_to_sinks(h, y, r0, r1, c));
+    }
+    DG_CUDA(cudaEventRecord(h->ev_d2h_done, cs[0]));
+    DG_CUDA(cudaStreamWaitEvent(s, h->ev_d2h_done, 0));
+    if (cs[1] != cs[0]) {
+      DG_CUDA(cudaEventRecord(h->ev_d2h_done2, cs[1]));
+      DG_CUDA(cudaStreamWaitEvent(s, h->ev_d2h_done2, 0));
+    }
   }
   DG_CUDA(cudaEventRecord(h->ev[3], s));
   h->timing_valid = false;

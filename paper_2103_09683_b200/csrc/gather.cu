@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <cstring>
+#include <vector>
 
 #include "common.cuh"
 #include "handle.cuh"
@@ -29,6 +30,21 @@ int dg_set_gather_targets(dg_handle* hh, double* const* targets, uint32_t n) {
   gt.row_off = h->row_begin;
   h->gt = gt;
   h->gt_zeroed = false;  // the next dose zero-fills this shard's rows of the new targets
+  return DG_OK;
+}
+
+int dg_set_block_targets(dg_handle* hh, double* const* targets, uint32_t n) {
+  dg::DeviceGuard device_guard;  // the caller's current device is restored on return
+  dg::Handle* h = reinterpret_cast<dg::Handle*>(hh);
+  if (!h) return DG_ERR_INVALID_CONFIG;
+  if (n > dg::kMaxGatherTargets || (n && !targets)) return DG_ERR_INVALID_CONFIG;
+  std::vector<const double*> dst(n);
+  std::vector<int> dev(n, -1);  // UVA copies (IPC mappings, own device)
+  for (uint32_t i = 0; i < n; ++i) {
+    if (!targets[i]) return DG_ERR_INVALID_CONFIG;
+    dst[i] = targets[i] + h->row_begin;
+  }
+  dg::set_block_sinks(h, dst.data(), dev.data(), n);
   return DG_OK;
 }
 

@@ -138,6 +138,13 @@ struct Handle {
   cudaEvent_t ev_d2h_done2 = nullptr;
   cudaEvent_t ev_tiles_start = nullptr, ev_d2h_done = nullptr;
   bool signal_blocks = false;  // this dose publishes block completion (host d, overlapped D2H)
+  // dg_multi PEER gather: device copies of this shard's rows (other devices' full d at this
+  // shard's offset); a device-d dose copies each row block there as soon as the tile kernel
+  // publishes it (copy engines, overlapped with the later blocks' tiles)
+  std::vector<double*> sink_ptr;
+  std::vector<int> sink_dev;
+  bool sink_overlap = false;  // (this dose)
+  bool sink_remote = false;   // some sink is on another device (overlap pays there)
 
   // fused d gather: every finished row also goes to each rank's full-d buffer (peer memory)
   GatherTargets gt = {};
@@ -233,6 +240,9 @@ int dispatch_mat(const Handle* h, F&& f) {
 
 typedef CUresult (*WaitValueFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 WaitValueFn wait_value_fn();
+// dg_multi: register the peer copies of this shard's rows (see sink_ptr); false if unused
+bool set_block_sinks(Handle* h, const double* const* dst, const int* dev, uint32_t n);
+int copy_to_sinks(Handle* h, const double* src, uint64_t r0, uint64_t r1, cudaStream_t c);
 
 // shared by dosegpu.cu, plan.cu and generator.cu
 int select_device(int32_t want, int* dev_out);

@@ -9,8 +9,9 @@
 // only when asked:
 //   * PEER: every shard's kernels write their rows straight into its own device's full-d buffer
 //     (y of that dg_dose = full_d + bounds[g]); the other devices' full d receive that range by
-//     cudaMemcpyPeerAsync on the shard's stream, i.e. the copy engines move it over NVLink /
-//     NVSwitch in large coalesced transfers right after the shard's kernels finish;
+//     cudaMemcpyPeerAsync, i.e. the copy engines move it over NVLink / NVSwitch in large
+//     coalesced transfers: row block by row block as the tile kernel publishes each block
+//     (cuStreamWaitValue32 on its completion flag), overlapped with the shard's later tiles;
 //   * NCCL: an allgatherv with no padding -- ncclGroupStart, for every shard g and every rank r
 //     ncclBroadcast(full_r + b_g, count nr_g, root g), ncclGroupEnd.
 // NCCL is loaded with dlopen on first use, so the library itself keeps no link-time dependency
@@ -156,6 +157,21 @@ int finish_multi(Multi* m) {
       if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return DG_ERR_CUDA_BASE + (int)e;
       cudaGetLastError();
     }
+  // PEER: every shard's dose copies each of its row blocks into the other devices' full d as soon
+  // as the tile kernel publishes the block (copy engines over NVLink / NVSwitch, overlapped with
+  // the shard's later tiles); plans without row blocks copy right after their kernels
+  if (m->gather == DG_GATHER_PEER)
+    for (uint32_t g = 0; g < m->n; ++g) {
+      std::vector<const double*> dst;
+      std::vector<int> dv;
+      for (uint32_t t = 0; t < m->n; ++t)
+        if (t != g && m->full[t] != m->full[g]) {
+          dst.push_back(m->full[t] + m->bounds[g]);
+          dv.push_back(m->dev[t]);
+        }
+      set_block_sinks(reinterpret_cast<Handle*>(m->shard[g]), dst.data(), dv.data(),
+                      static_cast<uint32_t>(dst.size()));
+    }
   if (m->gather == DG_GATHER_NCCL) {
     if (!nccl().ok) return DG_ERR_NO_NCCL;
     m->comm.assign(m->n, nullptr);
@@ -220,15 +236,7 @@ int multi_dose(Multi* m, const double* x, uint64_t x_len, double* y, uint32_t fl
   }
   // 3. gather
   if (m->gather == DG_GATHER_PEER) {
-    for (uint32_t g = 0; g < m->n; ++g) {
-      const uint64_t r0 = m->bounds[g], nr = m->bounds[g + 1] - r0;
-      if (!nr) continue;
-      DG_CUDA(cudaSetDevice(m->dev[g]));
-      for (uint32_t t = 0; t < m->n; ++t)
-        if (t != g && m->full[t] != m->full[g])
-          DG_CUDA(cudaMemcpyPeerAsync(m->full[t] + r0, m->dev[t], m->full[g] + r0, m->dev[g],
-                                      nr * sizeof(double), m->stream[g]));
-    }
+    // (the shards' doses above issued their copies: block by block, overlapped with their tiles)
     // device t's full d is complete once every shard's copies into it are: each stream waits
     // for the others' copy-done events before its "gathered" mark
     for (uint32_t g = 0; g < m->n; ++g) {

@@ -148,6 +148,7 @@ _SIGS = {
     "dg_debug_trace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]),
     "dg_seeded_vector": (None, [C.c_uint64, C.c_uint64, C.c_void_p]),
     "dg_set_gather_targets": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.c_uint32]),
+    "dg_set_block_targets": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.c_uint32]),
     "dg_ipc_alloc": (C.c_int, [C.c_uint64, C.c_int32, C.POINTER(C.c_void_p), C.c_void_p]),
     "dg_ipc_open": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]),
     "dg_ipc_close": (C.c_int, [C.c_void_p]),
@@ -336,6 +337,13 @@ class DoseEngine:
         each of these full-d device buffers (this rank's own and its peers' IPC mappings)."""
         arr = (C.c_void_p * max(len(ptrs), 1))(*[C.c_void_p(p) for p in ptrs])
         _check(_lib().dg_set_gather_targets(self._h, arr, len(ptrs)), "dg_set_gather_targets")
+
+    def set_block_targets(self, ptrs: Sequence[int]) -> None:
+        """The d gather by the copy engines: every later dose copies its rows, row block by row
+        block as the tile kernel finishes each block, into each of these full-d device buffers
+        (at their global row index)."""
+        arr = (C.c_void_p * max(len(ptrs), 1))(*[C.c_void_p(p) for p in ptrs])
+        _check(_lib().dg_set_block_targets(self._h, arr, len(ptrs)), "dg_set_block_targets")
 
     def kernel_times(self) -> list:
         """Per-launch CUDA-event times + algorithmic bytes of the last profiled dose."""

@@ -117,11 +117,12 @@ class ShardedDose:
             return gather_dose(y_local, self.bounds, group)
         return None
 
-    def enable_fused_gather(self, group=None) -> "FusedGather":
-        """Switch this shard to the fused gather (see FusedGather); returns it."""
+    def enable_fused_gather(self, group=None, mode: str = "epilogue") -> "FusedGather":
+        """Switch this shard to the fused gather (see FusedGather; mode "epilogue" or "blocks");
+        returns it."""
         if self.engine is None:
             raise ValueError("the fused gather needs the shard's DoseEngine")
-        self.fused = FusedGather(self.engine, self.bounds, self.device, group)
+        self.fused = FusedGather(self.engine, self.bounds, self.device, group, mode=mode)
         return self.fused
 
     def close(self):
@@ -142,9 +143,17 @@ class FusedGather:
     (NVLink / NVSwitch P2P stores), so the exchange overlaps the SpMV instead of following it as
     a separate NCCL all-gather.  After ``dose`` returns on every rank (stream synchronised, then
     a barrier), ``full`` holds the complete d on this rank.
+
+    ``mode="blocks"``: the same buffers, filled by the copy engines instead of the kernels'
+    epilogues -- each row block of this rank's d is copied to every rank's full d as soon as the
+    tile kernel publishes the block (``dg_set_block_targets``): coalesced DMA over NVLink,
+    overlapped with the later blocks' tiles, no SM time and no scalar remote stores.
     """
 
-    def __init__(self, engine: DoseEngine, bounds, device: int, group=None):
+    def __init__(self, engine: DoseEngine, bounds, device: int, group=None,
+                 mode: str = "epilogue"):
+        if mode not in ("epilogue", "blocks"):
+            raise ValueError(f"unknown fused-gather mode {mode!r}")
         import torch.distributed as dist
 
         from .dose import PeerBuffer
@@ -158,7 +167,11 @@ class FusedGather:
         self.peers = [None if g == me else PeerBuffer.open(h, n, device)
                       for g, h in enumerate(handles)]
         ptrs = [self.mine.ptr if g == me else self.peers[g].ptr for g in range(len(handles))]
-        engine.set_gather_targets(ptrs)
+        self.mode = mode
+        if mode == "blocks":
+            engine.set_block_targets(ptrs)
+        else:
+            engine.set_gather_targets(ptrs)
         self.full = self.mine.tensor()
 
     @staticmethod
@@ -225,7 +238,10 @@ class FusedGather:
         import torch.distributed as dist
 
         if self.engine is not None and self.engine._h:
-            self.engine.set_gather_targets([])
+            if self.mode == "blocks":
+                self.engine.set_block_targets([])
+            else:
+                self.engine.set_gather_targets([])
         # peers must stop writing into our buffer before it is freed
         if dist.is_initialized():
             dist.barrier(group=self.group)

@@ -1,7 +1,8 @@
 """torchrun worker for tests/test_fused_gather_gpu.py::test_fused_gather_two_processes_ipc.
 
 Each rank holds one nnz-balanced row shard of a generated matrix, registers every rank's full-d
-buffer (its own + the peer's CUDA IPC mapping) as gather targets and checks its full d against
+buffer (its own + the peer's CUDA IPC mapping) as gather targets (argv[2] "epilogue": stores from
+the dose kernels; "blocks": copy-engine copies per finished row block) and checks its full d against
 the single-device dose bit for bit, over several doses with different x."""
 import os
 import sys
@@ -14,14 +15,14 @@ import paper_2103_09683_b200 as dg
 from paper_2103_09683_b200.sharded import ShardedDose
 
 
-def main(out_dir: str) -> None:
+def main(out_dir: str, mode: str = "epilogue") -> None:
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(0)
     dist.init_process_group("gloo")
     p = dg.profiles.c1()
     p.rows = 400_000
     sd = ShardedDose.for_generated(p, rank=rank, world=world, device=0)
-    fg = sd.enable_fused_gather()
+    fg = sd.enable_fused_gather(mode=mode)
     y_local = torch.empty(sd.local_rows, dtype=torch.float64, device="cuda")
     with dg.DoseEngine.generate(p, device=0) as whole:
         for seed in (42, 5, 6):
@@ -41,4 +42,4 @@ def main(out_dir: str) -> None:
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], *(sys.argv[2:3]))

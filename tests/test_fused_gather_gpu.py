@@ -108,13 +108,53 @@ def test_gather_target_errors():
         assert buf.cpu().tolist() == [1.0, 0.0, 1.0, 0.0]
 
 
-def test_fused_gather_two_processes_ipc(tmp_path):
-    """Two ranks (gloo, both on cuda:0): IPC-mapped full-d buffers, each rank's kernels writing
-    into the other's.  The worker asserts bit-equality with the single-device d."""
+@pytest.mark.parametrize("blocks", ["4", "16"])
+def test_block_targets_bit_exact_host_and_device_d(monkeypatch, blocks):
+    """dg_set_block_targets: the shards' doses copy each finished row block into every full-d
+    buffer (copy engines, started by the tile kernel's block flags).  Device-resident and host d,
+    x alternating, NaN-prefilled targets: every target equals the single-device d bit for bit."""
+    import torch
+    monkeypatch.setenv("DG_BLOCKS", blocks)
+    p = dg.profiles.c1()
+    p.rows = 300_000
+    with dg.DoseEngine.generate(p) as whole:
+        lens = dg.generated_row_lengths(p, 0, p.rows)
+        b = dg.partition_lengths(lens, 3)
+        fulls = [torch.full((p.rows,), float("nan"), dtype=torch.float64, device="cuda")
+                 for _ in range(2)]
+        shards = [dg.DoseEngine.generate(p, row_begin=int(b[g]), row_end=int(b[g + 1]))
+                  for g in range(3)]
+        for s in shards:
+            s.set_block_targets([f.data_ptr() for f in fulls])
+        for it, seed in enumerate((42, 3, 4, 5)):
+            x = dg.seeded_vector(p.cols, seed)
+            want = bits(whole.dose(x))
+            xd = torch.from_numpy(x).cuda()
+            for g, s in enumerate(shards):
+                if it % 2:
+                    s.dose(x)  # host d
+                else:
+                    y = torch.empty(int(b[g + 1] - b[g]), dtype=torch.float64, device="cuda")
+                    s.dose_device(xd.data_ptr(), p.cols, y.data_ptr())
+            torch.cuda.synchronize()
+            for f in fulls:
+                assert np.array_equal(f.cpu().numpy().view(np.uint64), want), seed
+        for s in shards:
+            s.set_block_targets([])
+            s.close()
+
+
+@pytest.mark.parametrize("mode", ["epilogue", "blocks"])
+def test_fused_gather_two_processes_ipc(tmp_path, mode):
+    """Two ranks (gloo, both on cuda:0): IPC-mapped full-d buffers, each rank's kernels (mode
+    "epilogue") or copy engines (mode "blocks") writing into the other's.  The worker asserts
+    bit-equality with the single-device d."""
     env = dict(os.environ, PYTHONPATH=ROOT)
+    if mode == "blocks":
+        env["DG_BLOCKS"] = "8"  # several row blocks per shard: copies overlapped with the tiles
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr", "127.0.0.1", "--master-port", "29613",
-           os.path.join(ROOT, "tests", "fused_gather_worker.py"), str(tmp_path)]
+           "--master-addr", "127.0.0.1", "--master-port", "29613" if mode == "epilogue" else "29614",
+           os.path.join(ROOT, "tests", "fused_gather_worker.py"), str(tmp_path), mode]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     for g in range(2):

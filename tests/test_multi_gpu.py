@@ -58,6 +58,27 @@ def test_virtual_shards_match_single_device(port, liver, gather, n):
         assert t["ms_total"] > 0 and t["ms_kernels"] > 0
 
 
+@pytest.mark.parametrize("blocks", ["4", "16"])
+def test_peer_gather_overlapped_per_row_block(port, liver, monkeypatch, blocks):
+    """PEER gather with row blocks: each shard's dose copies every block into the other devices'
+    full d as soon as its tile kernel flags the block done, while later blocks are computed.  x
+    changes every dose, so a block copied before its rows were final would hold the previous
+    dose's values on some device."""
+    import torch
+    monkeypatch.setenv("DG_BLOCKS", blocks)
+    monkeypatch.setenv("DG_SINK_OVERLAP", "1")  # (same-device sinks copy after the kernels otherwise)
+    with dg.MultiDoseEngine.from_csr(to_dg(liver), [0, 0, 0], gather=dg.GATHER_PEER) as m:
+        for seed in (5, 6, 7, 8):
+            x = port.seeded_vector(liver.cols, seed)
+            want = bits(port.spmv_rowchunk(liver, x, 32, 4))
+            xd = torch.from_numpy(x).cuda()
+            m.dose_device(xd.data_ptr(), xd.numel())
+            for i in range(3):
+                full, _ = m.device_d(i)
+                assert np.array_equal(bits(_device_array(full, liver.rows)), want), (seed, i)
+            assert np.array_equal(bits(m.dose(x)), want)
+
+
 def test_device_x_and_repeated_doses(port, liver):
     import torch
     with dg.MultiDoseEngine.from_csr(to_dg(liver), [0, 0, 0, 0]) as m:
