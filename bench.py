@@ -435,7 +435,7 @@ def run_ours(args):
 
     # N > 1 (C2/C3): the d slices all-gathered over NCCL into the full d on every rank (8(e)),
     # timed separately from the sharded-resident step
-    gather_ms = fused_ms = 0.0
+    gather_ms = fused_ms = blocks_ms = 0.0
     if dist and bounds is not None:
         from paper_2103_09683_b200.sharded import gather_dose
         for _ in range(2):
@@ -455,37 +455,45 @@ def run_ours(args):
         # the same exchange fused into the dose kernels: rows stored into every rank's full d over
         # peer memory (CUDA IPC mappings), then a one-element all_reduce as the device-side
         # barrier that orders every rank's stores before the step ends
+        # mode "blocks": the same buffers filled by copy-engine DMA of each row block as the tile
+        # kernel finishes it (dg_set_block_targets)
         from paper_2103_09683_b200.sharded import FusedGather
         if FusedGather.preflight(local):  # same answer on every rank
-            fg = FusedGather(engines[0], bounds, local)
-            flag = torch.zeros(1, dtype=torch.float64, device="cuda")
+            for mode in ("epilogue", "blocks"):
+                fg = FusedGather(engines[0], bounds, local, mode=mode)
+                flag = torch.zeros(1, dtype=torch.float64, device="cuda")
 
-            def step_fused():
-                step()
-                dist.all_reduce(flag)
+                def step_fused():
+                    step()
+                    dist.all_reduce(flag)
 
-            for _ in range(2):
-                step_fused()
-            torch.cuda.synchronize()
-            dist.barrier()
-            fused_ms = timed(step_fused, e2e_steps)
-            dist.barrier()
-            assert torch.equal(fg.full.view(torch.int64), full[0].view(torch.int64)), \
-                "fused gather differs from the NCCL all-gather"
-            fg.close()
+                for _ in range(2):
+                    step_fused()
+                torch.cuda.synchronize()
+                dist.barrier()
+                t_mode = timed(step_fused, e2e_steps)
+                dist.barrier()
+                assert torch.equal(fg.full.view(torch.int64), full[0].view(torch.int64)), \
+                    f"fused gather ({mode}) differs from the NCCL all-gather"
+                fg.close()
+                if mode == "epilogue":
+                    fused_ms = t_mode
+                else:
+                    blocks_ms = t_mode
         else:
-            fused_ms = -1.0  # CUDA IPC unavailable between these processes: not measured
+            fused_ms = blocks_ms = -1.0  # CUDA IPC unavailable between these processes
 
     model_bytes = sum(e.info["model_bytes"] for e in engines)
     nnz = sum(e.info["nnz"] for e in engines)
     lrows = sum(e.info["rows"] for e in engines)
-    vals = torch.tensor([ms, e2e_ms, gather_ms, fused_ms], dtype=torch.float64, device="cuda")
+    vals = torch.tensor([ms, e2e_ms, gather_ms, fused_ms, blocks_ms], dtype=torch.float64,
+                        device="cuda")
     sums = torch.tensor([float(model_bytes), float(nnz), 8.0 * cols * len(engines), 8.0 * lrows],
                         dtype=torch.float64, device="cuda")
     if dist:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
         dist.all_reduce(sums, op=dist.ReduceOp.SUM)
-    ms, e2e_ms, gather_ms, fused_ms = vals.tolist()
+    ms, e2e_ms, gather_ms, fused_ms, blocks_ms = vals.tolist()
     total_bytes, total_nnz, h2d, d2h = sums.tolist()
     ms_step = ms / args.steps
     e2e_step_ms = e2e_ms / e2e_steps
@@ -561,6 +569,8 @@ def run_ours(args):
         "ms_per_step_gathered": (gather_ms / e2e_steps) if gather_ms else None,
         "ms_per_step_gathered_fused": (fused_ms / e2e_steps) if fused_ms > 0 else
                                       ("unavailable: CUDA IPC" if fused_ms < 0 else None),
+        "ms_per_step_gathered_blocks": (blocks_ms / e2e_steps) if blocks_ms > 0 else
+                                       ("unavailable: CUDA IPC" if blocks_ms < 0 else None),
         "clocks": clk,
     }
     if args.config == "c5":

@@ -43,6 +43,8 @@ def test_bench_two_ranks_orchestration():
              env={"DG_BENCH_ONE_DEVICE": "1"})
     assert d["n_gpus"] == 2 and d["scaling"] == "strong"
     assert d["ms_per_step_gathered"] > 0 and d["cpu_baseline"] is None
+    for k in ("ms_per_step_gathered_fused", "ms_per_step_gathered_blocks"):  # IPC gathers, both modes
+        assert d[k] == "unavailable: CUDA IPC" or d[k] > 0, (k, d[k])
     assert d["config"]["rows"] == 400000
 
 
