@@ -108,6 +108,28 @@ def test_gather_target_errors():
         assert buf.cpu().tolist() == [1.0, 0.0, 1.0, 0.0]
 
 
+@pytest.mark.parametrize("lane_width", [1, 8, 32, 64])
+def test_block_targets_every_lane_width(port, monkeypatch, lane_width):
+    """Block targets on plans without row blocks (lane widths != 32, split rows): the shard's d
+    is copied after its kernels; every target equals the reference's d bit for bit."""
+    import torch
+    monkeypatch.setenv("DG_BLOCKS", "4")
+    m = _wide_row_matrix(port, rows=1500)
+    x = port.seeded_vector(m.cols, 42)
+    want = port.spmv_rowchunk(m, x, lane_width, 4)
+    targets = [torch.full((m.rows,), float("nan"), dtype=torch.float64, device="cuda")
+               for _ in range(2)]
+    b = dg.partition_rows(m.row_ptr, 3)
+    for g in range(3):
+        with dg.DoseEngine.from_csr(to_dg(m), row_begin=int(b[g]), row_end=int(b[g + 1]),
+                                    lane_width=lane_width) as e:
+            e.set_block_targets([t.data_ptr() for t in targets])
+            e.dose(x)
+    torch.cuda.synchronize()
+    for t in targets:
+        assert np.array_equal(bits(t.cpu().numpy()), bits(want))
+
+
 @pytest.mark.parametrize("blocks", ["4", "16"])
 def test_block_targets_bit_exact_host_and_device_d(monkeypatch, blocks):
     """dg_set_block_targets: the shards' doses copy each finished row block into every full-d
