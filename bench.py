@@ -8,7 +8,8 @@ One step = one dose evaluation over the whole matrix (every rank's row shard).  
 BASELINE.json configs[1], C2 = 8M voxels x 40k spots, ~3.2e9 nnz, binary16 values, u16 indices,
 generated on the device (the reference's serial host generator would take ~7 min); x =
 ddm::seeded_vector(40000, 42).  The matrix (12.9 GB) is ~100x the 126 MB L2, so no flush is
-needed between steps ("inputs larger than L2").
+needed between steps ("inputs larger than L2").  --config c4 is the optimisation loop of
+SURVEY 8(d): step k doses x_k = seeded_vector(196608, 1000 + k) (8 x cycled).
 
 value    = SpMV effective GB/s = sum over ranks of ddm::traffic(dims, layout_of) bytes / step
            time (max over ranks, CUDA events, device-resident x/d).
