@@ -520,6 +520,9 @@ bool set_block_sinks(Handle* h, const double* const* dst, const int* dev, uint32
 // rows [r0, r1) of this shard's d (src: device) into every sink: peer copies between devices of
 // this process (dg_multi), plain UVA copies for CUDA-IPC mappings (sink_dev < 0)
 int copy_to_sinks(Handle* h, const double* src, uint64_t r0, uint64_t r1, cudaStream_t c) {
+  if (h->host_sink && r1 > r0)  // dg_multi with host d: this shard's slice of the caller's d
+    DG_CUDA(cudaMemcpyAsync(h->host_sink + r0, src + r0, (r1 - r0) * sizeof(double),
+                            cudaMemcpyDeviceToHost, c));
   for (size_t i = 0; i < h->sink_ptr.size() && r1 > r0; ++i) {
     if (h->sink_dev[i] >= 0)
       DG_CUDA(cudaMemcpyPeerAsync(h->sink_ptr[i] + r0, h->sink_dev[i], src + r0, h->device,
@@ -788,8 +791,9 @@ int dg_dose(dg_handle* hh, const double* x, uint64_t x_len, double* y, uint32_t 
   //  vs 1.98 after the kernels; DG_SINK_OVERLAP=1 forces it for tests)
   const char* fs = std::getenv("DG_SINK_OVERLAP");
   const bool force_sink = fs && *fs == '1';
-  h->sink_overlap = y_dev && block_plan && !h->sink_ptr.empty() && !h->profiling &&
-                    (h->sink_remote || force_sink);
+  const bool sinks = !h->sink_ptr.empty() || h->host_sink;
+  h->sink_overlap = y_dev && block_plan && sinks && !h->profiling &&
+                    (h->sink_remote || h->host_sink || force_sink);
   h->signal_blocks = overlap || h->sink_overlap;
   if (h->signal_blocks) ++h->epoch;
   DG_TRY(dg::run_kernels(h, d_x, d_y, s));
@@ -823,7 +827,7 @@ int dg_dose(dg_handle* hh, const double* x, uint64_t x_len, double* y, uint32_t 
   } else if (!y_dev && h->rows) {
     DG_CUDA(cudaMemcpyAsync(y, h->d_y, h->rows * sizeof(double), cudaMemcpyDeviceToHost, s));
     DG_TRY(dg::copy_to_sinks(h, h->d_y, 0, h->rows, s));
-  } else if (y_dev && h->rows && !h->sink_ptr.empty()) {
+  } else if (y_dev && h->rows && sinks) {
     // dg_multi PEER gather: block k of this shard's d goes to every other device's full d as
     // soon as its last tile is done (sink_overlap), or all of it after the kernels
     static const int n_cs = [] { const char* v = std::getenv("DG_D2H_STREAMS"); return v && *v == '1' ? 1 : 2; }();

@@ -145,6 +145,7 @@ struct Handle {
   std::vector<int> sink_dev;
   bool sink_overlap = false;  // (this dose)
   bool sink_remote = false;   // some sink is on another device (overlap pays there)
+  double* host_sink = nullptr;  // dg_multi, host d: this dose also downloads its rows here, block by block
 
   // fused d gather: every finished row also goes to each rank's full-d buffer (peer memory)
   GatherTargets gt = {};

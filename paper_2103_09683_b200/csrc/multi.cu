@@ -228,9 +228,24 @@ int multi_dose(Multi* m, const double* x, uint64_t x_len, double* y, uint32_t fl
   }
   // 2. every shard's dose, issued back to back (no host sync): the devices run concurrently;
   //    rows land in the shard device's full d at their global row
+  //    (host d: each shard's dose also downloads its slice of the caller's d row block by row
+  //    block as its tile kernel finishes each block -- over every device's own PCIe link,
+  //    overlapped with the later blocks)
+  //    Pinned host d only: a copy into pageable memory blocks the host thread until its block is
+  //    done, which would serialise the devices' launches -- pageable d is downloaded in step 4.
+  bool pinned = false;
+  if (y_host && m->rows) {
+    cudaPointerAttributes pa{};
+    pinned = cudaPointerGetAttributes(&pa, y) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+  }
   for (uint32_t g = 0; g < m->n; ++g) {
-    DG_TRY(dg_dose(m->shard[g], m->x[g], m->cols, m->full[g] + m->bounds[g],
-                   DG_X_ON_DEVICE | DG_Y_ON_DEVICE | DG_NO_SYNC, m->stream[g]));
+    Handle* hg = reinterpret_cast<Handle*>(m->shard[g]);
+    hg->host_sink = pinned ? y + m->bounds[g] : nullptr;
+    const int st = dg_dose(m->shard[g], m->x[g], m->cols, m->full[g] + m->bounds[g],
+                           DG_X_ON_DEVICE | DG_Y_ON_DEVICE | DG_NO_SYNC, m->stream[g]);
+    hg->host_sink = nullptr;
+    DG_TRY(st);
     DG_CUDA(cudaSetDevice(m->dev[g]));
     DG_CUDA(cudaEventRecord(m->ev[4 * g + 2], m->stream[g]));
   }
@@ -265,11 +280,12 @@ int multi_dose(Multi* m, const double* x, uint64_t x_len, double* y, uint32_t fl
     }
     DG_NCCL(nccl().group_end());
   }
-  // 4. the full d to the host: every device downloads its own slice concurrently
+  // 4. pageable host d: every device downloads its own slice concurrently (pinned host d was
+  //    downloaded block by block by the shards' doses in step 2)
   for (uint32_t g = 0; g < m->n; ++g) {
     DG_CUDA(cudaSetDevice(m->dev[g]));
     const uint64_t r0 = m->bounds[g], nr = m->bounds[g + 1] - r0;
-    if (y_host && nr)
+    if (y_host && !pinned && nr)
       DG_CUDA(cudaMemcpyAsync(y + r0, m->full[g] + r0, nr * sizeof(double), cudaMemcpyDeviceToHost,
                               m->stream[g]));
     DG_CUDA(cudaEventRecord(m->ev[4 * g + 3], m->stream[g]));

@@ -79,6 +79,27 @@ def test_peer_gather_overlapped_per_row_block(port, liver, monkeypatch, blocks):
             assert np.array_equal(bits(m.dose(x)), want)
 
 
+@pytest.mark.parametrize("gather", [dg.GATHER_NONE, dg.GATHER_PEER])
+@pytest.mark.parametrize("blocks", ["1", "8"])
+def test_pinned_host_d_downloaded_per_row_block(port, liver, monkeypatch, gather, blocks):
+    """Pinned host d: each shard's dose downloads its slice row block by row block as its tile
+    kernel finishes each block (over each device's own link).  x alternates, host d prefilled
+    with NaN: every dose's host d equals the reference's bit for bit."""
+    import torch
+    monkeypatch.setenv("DG_BLOCKS", blocks)
+    with dg.MultiDoseEngine.from_csr(to_dg(liver), [0, 0, 0], gather=gather) as m:
+        yh = torch.full((liver.rows,), float("nan"), dtype=torch.float64).pin_memory()
+        for seed in (11, 12, 13):
+            x = port.seeded_vector(liver.cols, seed)
+            xh = torch.from_numpy(x).pin_memory()
+            m.dose_host_ptrs(xh.data_ptr(), liver.cols, yh.data_ptr())
+            assert np.array_equal(bits(yh.numpy()), bits(port.spmv_rowchunk(liver, x, 32, 4))), seed
+            if gather == dg.GATHER_PEER:
+                for i in range(3):
+                    full, _ = m.device_d(i)
+                    assert np.array_equal(bits(_device_array(full, liver.rows)), bits(yh.numpy()))
+
+
 def test_device_x_and_repeated_doses(port, liver):
     import torch
     with dg.MultiDoseEngine.from_csr(to_dg(liver), [0, 0, 0, 0]) as m:
