@@ -798,25 +798,32 @@ int dg_dose(dg_handle* hh, const double* x, uint64_t x_len, double* y, uint32_t 
   if (h->signal_blocks) ++h->epoch;
   DG_TRY(dg::run_kernels(h, d_x, d_y, s));
   DG_CUDA(cudaEventRecord(h->ev[2], s));
-  if (overlap) {
-    // blocks alternate between two copy streams (two copy engines: DG_D2H_STREAMS=1 for one)
-    static const int n_d2h = [] { const char* v = std::getenv("DG_D2H_STREAMS"); return v && *v == '1' ? 1 : 2; }();
-    cudaStream_t cs[2] = {h->d2h_stream, n_d2h > 1 ? h->d2h_stream2 : h->d2h_stream};
+  // Row blocks out of the device d `src` on two copy streams (blocks alternate: two copy engines;
+  // DG_D2H_STREAMS=1 for one): into the host d (host_dst, may be null) and every sink.  Per block,
+  // each copy waits for the tile kernel's completion flag of that block (per_block), or the whole
+  // d follows the kernels.  The dose's stream waits for both copy streams at the end.
+  auto copy_out = [&](const double* src, double* host_dst, bool per_block) -> int {
+    static const int n_cs = [] { const char* v = std::getenv("DG_D2H_STREAMS"); return v && *v == '1' ? 1 : 2; }();
+    cudaStream_t cs[2] = {h->d2h_stream, n_cs > 1 ? h->d2h_stream2 : h->d2h_stream};
+    if (!per_block) DG_CUDA(cudaEventRecord(h->ev_tiles_start, s));  // (after the kernels)
     DG_CUDA(cudaStreamWaitEvent(cs[0], h->ev_tiles_start, 0));
     if (cs[1] != cs[0]) DG_CUDA(cudaStreamWaitEvent(cs[1], h->ev_tiles_start, 0));
-    for (uint32_t k = 0; k < h->n_blocks; ++k) {
-      const uint64_t r0 = h->blk_row0[k], r1 = h->blk_row0[k + 1];
+    const uint32_t nb = per_block ? h->n_blocks : 1;
+    for (uint32_t k = 0; k < nb; ++k) {
+      const uint64_t r0 = per_block ? h->blk_row0[k] : 0;
+      const uint64_t r1 = per_block ? h->blk_row0[k + 1] : h->rows;
       if (r1 == r0) continue;
       cudaStream_t c = cs[k & 1];
-      if (h->blk_tiles[k]) {
+      if (per_block && h->blk_tiles[k]) {
         const CUresult cr = dg::wait_value_fn()(
             reinterpret_cast<CUstream>(c),
             reinterpret_cast<CUdeviceptr>(h->d_blk_flag + k), h->epoch, CU_STREAM_WAIT_VALUE_GEQ);
         if (cr != CUDA_SUCCESS) return DG_ERR_CUDA_BASE + static_cast<int>(cudaErrorUnknown);
       }
-      DG_CUDA(cudaMemcpyAsync(y + r0, h->d_y + r0, (r1 - r0) * sizeof(double),
-                              cudaMemcpyDeviceToHost, c));
-      DG_TRY(dg::copy_to_sinks(h, h->d_y, r0, r1, c));
+      if (host_dst)
+        DG_CUDA(cudaMemcpyAsync(host_dst + r0, src + r0, (r1 - r0) * sizeof(double),
+                                cudaMemcpyDeviceToHost, c));
+      DG_TRY(dg::copy_to_sinks(h, src, r0, r1, c));
     }
     DG_CUDA(cudaEventRecord(h->ev_d2h_done, cs[0]));
     DG_CUDA(cudaStreamWaitEvent(s, h->ev_d2h_done, 0));
@@ -824,42 +831,17 @@ int dg_dose(dg_handle* hh, const double* x, uint64_t x_len, double* y, uint32_t 
       DG_CUDA(cudaEventRecord(h->ev_d2h_done2, cs[1]));
       DG_CUDA(cudaStreamWaitEvent(s, h->ev_d2h_done2, 0));
     }
+    return DG_OK;
+  };
+  if (overlap) {  // host d, downloaded block by block while the tile kernel works on later blocks
+    DG_TRY(copy_out(h->d_y, y, true));
   } else if (!y_dev && h->rows) {
     DG_CUDA(cudaMemcpyAsync(y, h->d_y, h->rows * sizeof(double), cudaMemcpyDeviceToHost, s));
     DG_TRY(dg::copy_to_sinks(h, h->d_y, 0, h->rows, s));
   } else if (y_dev && h->rows && sinks) {
-    // dg_multi PEER gather: block k of this shard's d goes to every other device's full d as
-    // soon as its last tile is done (sink_overlap), or all of it after the kernels
-    static const int n_cs = [] { const char* v = std::getenv("DG_D2H_STREAMS"); return v && *v == '1' ? 1 : 2; }();
-    cudaStream_t cs[2] = {h->d2h_stream, n_cs > 1 ? h->d2h_stream2 : h->d2h_stream};
-    if (h->sink_overlap) {
-      DG_CUDA(cudaStreamWaitEvent(cs[0], h->ev_tiles_start, 0));
-      if (cs[1] != cs[0]) DG_CUDA(cudaStreamWaitEvent(cs[1], h->ev_tiles_start, 0));
-    } else {
-      DG_CUDA(cudaEventRecord(h->ev_tiles_start, s));  // (after the kernels)
-      DG_CUDA(cudaStreamWaitEvent(cs[0], h->ev_tiles_start, 0));
-      if (cs[1] != cs[0]) DG_CUDA(cudaStreamWaitEvent(cs[1], h->ev_tiles_start, 0));
-    }
-    const uint32_t nb = h->sink_overlap ? h->n_blocks : 1;
-    for (uint32_t k = 0; k < nb; ++k) {
-      const uint64_t r0 = h->sink_overlap ? h->blk_row0[k] : 0;
-      const uint64_t r1 = h->sink_overlap ? h->blk_row0[k + 1] : h->rows;
-      if (r1 == r0) continue;
-      cudaStream_t c = cs[k & 1];
-      if (h->sink_overlap && h->blk_tiles[k]) {
-        const CUresult cr = dg::wait_value_fn()(
-            reinterpret_cast<CUstream>(c),
-            reinterpret_cast<CUdeviceptr>(h->d_blk_flag + k), h->epoch, CU_STREAM_WAIT_VALUE_GEQ);
-        if (cr != CUDA_SUCCESS) return DG_ERR_CUDA_BASE + static_cast<int>(cudaErrorUnknown);
-      }
-      DG_TRY(dg::copy_to_sinks(h, y, r0, r1, c));
-    }
-    DG_CUDA(cudaEventRecord(h->ev_d2h_done, cs[0]));
-    DG_CUDA(cudaStreamWaitEvent(s, h->ev_d2h_done, 0));
-    if (cs[1] != cs[0]) {
-      DG_CUDA(cudaEventRecord(h->ev_d2h_done2, cs[1]));
-      DG_CUDA(cudaStreamWaitEvent(s, h->ev_d2h_done2, 0));
-    }
+    // device d with sinks (dg_multi PEER gather / host d, block targets): block k as soon as its
+    // last tile is done (sink_overlap), or all of d after the kernels
+    DG_TRY(copy_out(y, nullptr, h->sink_overlap));
   }
   DG_CUDA(cudaEventRecord(h->ev[3], s));
   h->timing_valid = false;
